@@ -1,0 +1,1092 @@
+// fdg_api.cu — host side of the C ABI (include/fdg.h).
+//
+// Mirrors the reference's operator / preconditioner / Krylov / ADMM entry
+// points (/root/reference/proj/include/fdeopt/{toeplitz,circulant,admm}.hpp)
+// over device-resident state.  Per Krylov iteration only two scalars (p^T S p
+// and |r|^2) cross to the host, for the reference's convergence and
+// breakdown checks (admm.cpp:143-158).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/fdg.h"
+#include "fdg_internal.h"
+
+using fdg::AxisSym;
+using fdg::LaunchCounter;
+using fdg::PcTables;
+using fdg::RedSlot;
+using fdg::TimeFactor;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_num = FDG_NUM_NONE;
+
+struct Error {
+  fdg_status code;
+  std::string msg;
+  int num = FDG_NUM_NONE;
+};
+
+[[noreturn]] void fail(fdg_status code, const std::string& msg, int num = FDG_NUM_NONE) {
+  throw Error{code, msg, num};
+}
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(FDG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+fdg_status guard(F&& f) {
+  try {
+    f();
+    g_num = FDG_NUM_NONE;
+    return FDG_OK;
+  } catch (const Error& e) {
+    g_err = e.msg;
+    g_num = e.num;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return FDG_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return FDG_EINVAL;
+  }
+}
+
+// ------------------------------------------------------- device buffers
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t b) { alloc(b); }
+  void alloc(size_t b) {
+    release();
+    if (b == 0) b = 8;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      fail(e == cudaErrorMemoryAllocation ? FDG_ENOMEM : FDG_ECUDA,
+           std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    bytes = b;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  double* d() const { return static_cast<double*>(p); }
+  double2* c() const { return static_cast<double2*>(p); }
+};
+
+bool is_pow2(long v) { return v >= 1 && (v & (v - 1)) == 0; }
+int pow2_ceil(long v) {
+  int L = 1;
+  while (L < v) L <<= 1;
+  return L;
+}
+
+// ------------------------------------------------- host setup arithmetic
+const long double kPi = 3.141592653589793238462643383279502884L;
+
+std::vector<double> twiddles(int L) {
+  std::vector<double> w(2 * (size_t)L);
+  for (int k = 0; k < L; ++k) {
+    long double a = -2.0L * kPi * (long double)k / (long double)L;
+    double c = (double)cosl(a), s = (double)sinl(a);
+    if (4 * k == L) { c = 0.0; s = -1.0; }
+    if (2 * k == L) { c = -1.0; s = 0.0; }
+    if (4 * k == 3 * L) { c = 0.0; s = 1.0; }
+    if (k == 0) { c = 1.0; s = 0.0; }
+    w[2 * k] = c;
+    w[2 * k + 1] = s;
+  }
+  return w;
+}
+
+// Full length-L spectrum of the circulant embedding of a Toeplitz factor:
+// c[k] = col[k] (k < n), c[L-k] = row[k] (0 < k < n)  (toeplitz.cpp:46-58 with
+// L >= 2n-1 instead of exactly 2n).  Direct sum in long double.
+std::vector<double> embed_symbol_full(const std::vector<double>& col, const std::vector<double>& row, int L) {
+  const int n = (int)col.size();
+  std::vector<long double> cs(L), sn(L);
+  for (int k = 0; k < L; ++k) {
+    const long double a = -2.0L * kPi * (long double)k / (long double)L;
+    cs[k] = cosl(a);
+    sn[k] = sinl(a);
+  }
+  std::vector<std::pair<int, long double>> nz;
+  for (int k = 0; k < n; ++k)
+    if (col[k] != 0.0) nz.push_back({k, (long double)col[k]});
+  for (int k = 1; k < n; ++k)
+    if (row[k] != 0.0) nz.push_back({L - k, (long double)row[k]});
+  std::vector<double> out(2 * (size_t)L);
+  for (int f = 0; f < L; ++f) {
+    long double re = 0.0L, im = 0.0L;
+    for (auto& [k, v] : nz) {
+      const int idx = (int)(((long long)f * k) % L);
+      re += v * cs[idx];
+      im += v * sn[idx];
+    }
+    out[2 * f] = (double)re;
+    out[2 * f + 1] = (double)im;
+  }
+  return out;
+}
+
+// circulant.cpp:10-26: T. Chan first column and its DFT (direct, long double).
+void tchan_host(int n, const double* col, const double* row, double* first_col, double* eigs) {
+  std::vector<double> c(n);
+  c[0] = col[0];
+  for (int i = 1; i < n; ++i) c[i] = ((n - i) * col[i] + i * row[n - i]) / n;
+  if (first_col) std::memcpy(first_col, c.data(), sizeof(double) * n);
+  for (int j = 0; j < n; ++j) {
+    long double re = 0.0L, im = 0.0L;
+    for (int k = 0; k < n; ++k) {
+      const long long jk = ((long long)j * k) % n;
+      const long double a = -2.0L * kPi * (long double)jk / (long double)n;
+      re += (long double)c[k] * cosl(a);
+      im += (long double)c[k] * sinl(a);
+    }
+    eigs[2 * j] = (double)re;
+    eigs[2 * j + 1] = (double)im;
+  }
+}
+
+std::vector<double> frac_coeffs_host(double order, int count) {
+  const bool valid = (order > 0.0 && order < 1.0) || (order > 1.0 && order < 2.0);
+  if (!valid) fail(FDG_EINVAL, "fractional order must lie in (0,1) or (1,2), got " + std::to_string(order));
+  if (count < 1) fail(FDG_EINVAL, "coefficient count must be >= 1");
+  std::vector<double> g(count);
+  g[0] = 1.0;
+  for (int k = 1; k < count; ++k) g[k] = (1.0 - (order + 1.0) / k) * g[k - 1];
+  return g;
+}
+
+}  // namespace
+
+// ====================================================================== ctx
+struct fdg_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  LaunchCounter lc;
+  // reduction infrastructure shared by every handle of this context (all
+  // work is ordered on one stream)
+  DevBuf partials;
+  DevBuf counters;
+  size_t partial_cap = 0;
+  double* pinned = nullptr;  // host staging for scalars
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+
+  void set_device() const { ck(cudaSetDevice(device), "cudaSetDevice"); }
+  void ensure_partials(size_t cap) {
+    if (cap <= partial_cap) return;
+    partials.alloc(sizeof(double) * 4 * cap);
+    partial_cap = cap;
+  }
+};
+
+namespace {
+
+// Device scalar block layout (per handle that reduces).
+enum Scal {
+  S_NB = 0,   // |rhs|^2
+  S_XX,       // |x|^2
+  S_RZ0,      // r.z ping
+  S_RZ1,      // r.z pong
+  S_PQ,       // p^T S p
+  S_RR,       // |r|^2
+  S_RR2,      // |r|^2 of the true residual
+  S_ADMM,     // 4: r_eq, r_y, r_v, bad
+  S_DINF = S_ADMM + 4,  // 2
+  S_OBJ = S_DINF + 2,   // 2
+  S_DOT = S_OBJ + 2,
+  S_COUNT
+};
+
+struct Scalars {
+  DevBuf vals;      // double[S_COUNT]
+  DevBuf counters;  // unsigned[S_COUNT]
+  fdg_ctx ctx = nullptr;
+  void init(fdg_ctx c) {
+    ctx = c;
+    vals.alloc(sizeof(double) * S_COUNT);
+    counters.alloc(sizeof(unsigned) * S_COUNT);
+    ck(cudaMemset(vals.p, 0, sizeof(double) * S_COUNT), "memset");
+    ck(cudaMemset(counters.p, 0, sizeof(unsigned) * S_COUNT), "memset");
+  }
+  double* at(int s) const { return vals.d() + s; }
+  RedSlot slot(int s) const {
+    return RedSlot{ctx->partials.d(), static_cast<unsigned*>(counters.p) + s, vals.d() + s};
+  }
+  // synchronous read of [s, s+cnt)
+  void read(int s, int cnt, double* out) const {
+    ck(cudaMemcpyAsync(ctx->pinned, vals.d() + s, sizeof(double) * cnt, cudaMemcpyDeviceToHost, ctx->stream),
+       "scalar D2H");
+    ck(cudaStreamSynchronize(ctx->stream), "stream sync");
+    std::memcpy(out, ctx->pinned, sizeof(double) * cnt);
+  }
+};
+
+}  // namespace
+
+// ================================================================ operator
+struct fdg_op_s {
+  fdg_ctx ctx = nullptr;
+  int nt = 0, n1 = 0, n2 = 0;
+  double psi = 1.0;
+  std::vector<double> tcol, trow, c1, r1, c2, r2;
+  DevBuf sym1, tw1, sym2, tw2, symt, symt_adj, twt;
+  AxisSym ax1, ax2;
+  TimeFactor tf;
+  size_t N() const { return (size_t)nt * n1 * n2; }
+  double scale1() const { return -psi / ax1.L; }
+  double scale2() const { return -psi / ax2.L; }
+};
+
+namespace {
+
+void upload(DevBuf& b, const std::vector<double>& h, cudaStream_t st) {
+  b.alloc(sizeof(double) * h.size());
+  ck(cudaMemcpyAsync(b.p, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, st), "H2D");
+  ck(cudaStreamSynchronize(st), "sync");
+}
+
+void build_axis(fdg_op_s* op, AxisSym& ax, DevBuf& sym, DevBuf* sym_adj, DevBuf& tw, const std::vector<double>& col,
+                const std::vector<double>& row) {
+  const int n = (int)col.size();
+  const int L = std::max(2, pow2_ceil(2L * n - 1));
+  if (L > 2048) fail(FDG_EUNSUPPORTED, "fdg: factor size " + std::to_string(n) + " exceeds the compiled kernel set (n <= 1024)");
+  ax.n = n;
+  ax.L = L;
+  upload(sym, embed_symbol_full(col, row, L), op->ctx->stream);
+  upload(tw, twiddles(L), op->ctx->stream);
+  ax.sym = sym.c();
+  ax.tw = tw.c();
+  ax.sym_adj = ax.sym;
+  if (sym_adj) {
+    upload(*sym_adj, embed_symbol_full(row, col, L), op->ctx->stream);
+    ax.sym_adj = sym_adj->c();
+  }
+}
+
+// B x into out (x != out): row pass (x2 + stencil) then x1 column pass
+// (in place on out), then the general time pass if any.
+void op_apply_dev(fdg_op_s* op, const double* x, double* out, bool adjoint) {
+  cudaStream_t st = op->ctx->stream;
+  LaunchCounter* lc = &op->ctx->lc;
+  ck(fdg::launch_row_apply(st, lc, x, out, op->nt, op->n1, op->n2, op->ax2, op->scale2(), op->tf, op->psi, adjoint),
+     "row pass");
+  ck(fdg::launch_col_acc(st, lc, x, out, out, op->nt, op->n1, op->n2, op->ax1, op->scale1(), false), "x1 pass");
+  if (op->tf.kind == 2)
+    ck(fdg::launch_col_acc(st, lc, x, out, out, 1, op->nt, op->n1 * op->n2, op->tf.fft, op->psi / op->tf.fft.L,
+                           adjoint),
+       "t pass");
+}
+
+}  // namespace
+
+// ================================================================== pc
+struct fdg_pc_s {
+  fdg_ctx ctx = nullptr;
+  int nt = 0, n1 = 0, n2 = 0;
+  double psi = 1.0, rho = 1.0, delta = 1.0, gamma = 1.0;
+  DevBuf lt, l1, l2, twt, tw1, tw2;
+  DevBuf work;  // N doubles (standalone solve)
+  PcTables tab;
+  size_t N() const { return (size_t)nt * n1 * n2; }
+};
+
+namespace {
+
+// z = S~^{-1} r via Hartley passes x2, x1, t(+divide), x1, x2.
+// h may alias z (not r).  rdot != null: reduce r.z into red.
+void pc_apply_dev(fdg_pc_s* pc, const double* r, double* z, double* h, const double* rdot, RedSlot red) {
+  cudaStream_t st = pc->ctx->stream;
+  LaunchCounter* lc = &pc->ctx->lc;
+  const int F = pc->nt * pc->n1;
+  RedSlot none{};
+  ck(fdg::launch_hartley_row(st, lc, r, h, F, pc->n2, pc->tab.tw_2, nullptr, none), "pc x2 fwd");
+  ck(fdg::launch_hartley_col(st, lc, h, pc->nt, pc->n1, pc->n2, pc->tab.tw_1), "pc x1 fwd");
+  ck(fdg::launch_t_filter(st, lc, h, pc->tab), "pc t filter");
+  ck(fdg::launch_hartley_col(st, lc, h, pc->nt, pc->n1, pc->n2, pc->tab.tw_1), "pc x1 inv");
+  ck(fdg::launch_hartley_row(st, lc, h, z, F, pc->n2, pc->tab.tw_2, rdot, red), "pc x2 inv");
+}
+
+}  // namespace
+
+// ================================================================= ADMM
+struct fdg_admm_s {
+  fdg_op_s* op = nullptr;
+  fdg_pc_s* pc = nullptr;
+  fdg_admm_desc desc{};
+  size_t N = 0, slice = 0;
+  int nt = 0;
+  double psi = 1.0, v_lo = 0, v_hi = 0;
+  // per-slice work (AdmmWork vectors are time-block constant, admm.cpp:52-79)
+  std::vector<double> h_diag_j, h_diag_j2, h_m2, h_a2inv;
+  DevBuf diag_j, diag_j2, m2, inv_m2, a2inv, a1;
+  // state (AdmmState admm.hpp:28-32) and work vectors
+  DevBuf y, v, z_y, z_v, p, w_y, w_v, ybar, By;
+  DevBuf rhs, r_cache, tmp;
+  DevBuf r, z, d, u, w, vp;  // PCG: residual, preconditioned residual, direction, scratch
+  Scalars sc;
+  double inner_tol = 0.0;
+  bool converged = false;
+  int stagnations = 0;
+  int iteration = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
+};
+
+namespace {
+
+fdg::AdmmScalars admm_scalars(const fdg_admm_s* a) {
+  return fdg::AdmmScalars{a->desc.rho, a->desc.delta, a->psi, a->desc.y_lo, a->desc.y_hi, a->v_lo, a->v_hi};
+}
+
+// q = S x (admm.cpp:87-98), fused: row(x) -> u; col(x,u) -> w, vp (+pq);
+// row(w, vp) -> q.  pq lands in S_PQ.
+void apply_S_dev(fdg_admm_s* a, const double* x, double* q) {
+  fdg_op_s* op = a->op;
+  cudaStream_t st = op->ctx->stream;
+  LaunchCounter* lc = &op->ctx->lc;
+  const TimeFactor& tf = op->tf;
+  TimeFactor none_tf;
+  ck(fdg::launch_row_apply(st, lc, x, a->u.d(), op->nt, op->n1, op->n2, op->ax2, op->scale2(),
+                           tf.kind == 1 ? tf : none_tf, op->psi, false),
+     "S row");
+  if (tf.kind == 2)
+    ck(fdg::launch_col_acc(st, lc, x, a->u.d(), a->u.d(), 1, op->nt, op->n1 * op->n2, tf.fft, op->psi / tf.fft.L,
+                           false),
+       "S t fwd");
+  ck(fdg::launch_col_s_mid(st, lc, x, a->u.d(), a->w.d(), a->vp.d(), op->nt, op->n1, op->n2, op->ax1, op->scale1(),
+                           a->inv_m2.d(), a->a1.d(), a->sc.slot(S_PQ)),
+     "S col");
+  if (tf.kind == 2)
+    ck(fdg::launch_col_acc(st, lc, a->w.d(), a->vp.d(), a->vp.d(), 1, op->nt, op->n1 * op->n2, tf.fft,
+                           op->psi / tf.fft.L, true),
+       "S t adj");
+  ck(fdg::launch_row_s_out(st, lc, a->w.d(), a->vp.d(), q, nullptr, op->nt, op->n1, op->n2, op->ax2, op->scale2(),
+                           tf.kind == 1 ? tf : none_tf, op->psi, nullptr, nullptr, RedSlot{}),
+     "S row adj");
+}
+
+// Search-direction product fused with the residual update:
+// r -= (rz/pq) S d ; reduces |r|^2 into S_RR and p^T S p into S_PQ.
+void s_and_update(fdg_admm_s* a, const double* dd, const double* rz_slot) {
+  fdg_op_s* op = a->op;
+  cudaStream_t st = op->ctx->stream;
+  LaunchCounter* lc = &op->ctx->lc;
+  const TimeFactor& tf = op->tf;
+  TimeFactor none_tf;
+  ck(fdg::launch_row_apply(st, lc, dd, a->u.d(), op->nt, op->n1, op->n2, op->ax2, op->scale2(),
+                           tf.kind == 1 ? tf : none_tf, op->psi, false),
+     "K1 row");
+  if (tf.kind == 2)
+    ck(fdg::launch_col_acc(st, lc, dd, a->u.d(), a->u.d(), 1, op->nt, op->n1 * op->n2, tf.fft, op->psi / tf.fft.L,
+                           false),
+       "K1 t");
+  ck(fdg::launch_col_s_mid(st, lc, dd, a->u.d(), a->w.d(), a->vp.d(), op->nt, op->n1, op->n2, op->ax1, op->scale1(),
+                           a->inv_m2.d(), a->a1.d(), a->sc.slot(S_PQ)),
+     "K2 col");
+  if (tf.kind == 2)
+    ck(fdg::launch_col_acc(st, lc, a->w.d(), a->vp.d(), a->vp.d(), 1, op->nt, op->n1 * op->n2, tf.fft,
+                           op->psi / tf.fft.L, true),
+       "K2 t");
+  ck(fdg::launch_row_s_out(st, lc, a->w.d(), a->vp.d(), nullptr, a->r.d(), op->nt, op->n1, op->n2, op->ax2,
+                           op->scale2(), tf.kind == 1 ? tf : none_tf, op->psi, rz_slot, a->sc.at(S_PQ),
+                           a->sc.slot(S_RR)),
+     "K3 row");
+}
+
+// pcg (admm.cpp:121-169) with apply = apply_S, precond = pc.solve.
+fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, int max_inner) {
+  fdg_ctx ctx = a->op->ctx;
+  cudaStream_t st = ctx->stream;
+  LaunchCounter* lc = &ctx->lc;
+  const size_t N = a->N;
+  Scalars& sc = a->sc;
+  fdg_pcg_result res{0, 0, 0.0, 0.0};
+  ck(cudaEventRecord(a->e0, st), "event");
+  double h[2];
+  ck(fdg::launch_dot(st, lc, rhs, nullptr, N, sc.slot(S_NB)), "nb");
+  ck(fdg::launch_dot(st, lc, x, nullptr, N, sc.slot(S_XX)), "xx");
+  sc.read(S_NB, 2, h);
+  const double nb = std::sqrt(h[0]);
+  auto finish = [&]() {
+    ck(cudaEventRecord(a->e1, st), "event");
+    ck(cudaEventSynchronize(a->e1), "event sync");
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, a->e0, a->e1), "elapsed");
+    res.ms = ms;
+  };
+  if (nb == 0.0) {
+    ck(fdg::launch_fill(st, lc, x, 0.0, N), "fill");
+    res = {0, 1, 0.0, 0.0};
+    finish();
+    return res;
+  }
+  if (std::sqrt(h[1]) == 0.0) {
+    ck(fdg::launch_copy(st, lc, a->r.d(), rhs, N), "r = b");
+  } else {
+    apply_S_dev(a, x, a->z.d());
+    ck(fdg::launch_residual(st, lc, a->r.d(), rhs, a->z.d(), N, sc.slot(S_RR2)), "r = b - Ax");
+  }
+  int cur = S_RZ0, nxt = S_RZ1;
+  pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(cur));
+  ck(fdg::launch_copy(st, lc, a->d.d(), a->z.d(), N), "p = z");
+  for (int it = 1; it <= max_inner; ++it) {
+    s_and_update(a, a->d.d(), sc.at(cur));
+    double pr[2];
+    sc.read(S_PQ, 2, pr);  // S_PQ, S_RR adjacent
+    const double pq = pr[0];
+    if (!std::isfinite(pq) || pq <= 0.0)
+      fail(FDG_ENUMERIC, "pcg: operator lost positive definiteness", FDG_NUM_PD_LOSS);
+    double rn = std::sqrt(pr[1]);
+    if (!std::isfinite(rn)) fail(FDG_ENUMERIC, "pcg: non-finite residual", FDG_NUM_NONFINITE_RESIDUAL);
+    bool x_done = false;
+    if (rn <= tol * nb) {
+      // confirm with the true residual (admm.cpp:152-158)
+      ck(fdg::launch_axpy_dev(st, lc, x, a->d.d(), N, sc.at(cur), sc.at(S_PQ)), "x += a p");
+      x_done = true;
+      apply_S_dev(a, x, a->z.d());
+      ck(fdg::launch_residual(st, lc, a->r.d(), rhs, a->z.d(), N, sc.slot(S_RR2)), "r = b - Ax");
+      double rr2;
+      sc.read(S_RR2, 1, &rr2);
+      rn = std::sqrt(rr2);
+      if (rn <= tol * nb) {
+        res = {it, 1, rn / nb, 0.0};
+        finish();
+        return res;
+      }
+    }
+    pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(nxt));
+    // x += (rz/pq) p ; p = z + (rz'/rz) p  (admm.cpp:148-150, 161-163)
+    ck(fdg::launch_cg_update(st, lc, x, a->d.d(), a->z.d(), N, sc.at(cur), sc.at(S_PQ), sc.at(nxt), sc.at(cur),
+                             !x_done),
+       "cg update");
+    std::swap(cur, nxt);
+  }
+  // cap: true relative residual (admm.cpp:165-168)
+  apply_S_dev(a, x, a->z.d());
+  ck(fdg::launch_residual(st, lc, a->u.d(), rhs, a->z.d(), N, sc.slot(S_RR2)), "res");
+  double rr2;
+  sc.read(S_RR2, 1, &rr2);
+  res = {max_inner, 0, std::sqrt(rr2) / nb, 0.0};
+  finish();
+  return res;
+}
+
+// build_rhs (admm.cpp:100-119)
+void build_rhs_dev(fdg_admm_s* a, double* rhs, double* r_cache) {
+  cudaStream_t st = a->op->ctx->stream;
+  LaunchCounter* lc = &a->op->ctx->lc;
+  const auto s = admm_scalars(a);
+  ck(fdg::launch_rhs_pre(st, lc, s, a->p.d(), a->w_v.d(), a->z_v.d(), a->a2inv.d(), a->m2.d(), r_cache, a->tmp.d(),
+                         a->slice, a->N),
+     "rhs pre");
+  op_apply_dev(a->op, a->tmp.d(), rhs, true);
+  ck(fdg::launch_rhs_post(st, lc, s, rhs, a->ybar.d(), a->w_y.d(), a->z_y.d(), a->diag_j.d(), a->slice, a->N),
+     "rhs post");
+}
+
+double* field_dev(fdg_admm_s* a, int f) {
+  switch (f) {
+    case FDG_F_Y: return a->y.d();
+    case FDG_F_V: return a->v.d();
+    case FDG_F_ZY: return a->z_y.d();
+    case FDG_F_ZV: return a->z_v.d();
+    case FDG_F_P: return a->p.d();
+    case FDG_F_WY: return a->w_y.d();
+    case FDG_F_WV: return a->w_v.d();
+    case FDG_F_YBAR: return a->ybar.d();
+    case FDG_F_BY: return a->By.d();
+    default: return nullptr;
+  }
+}
+
+const std::vector<double>* field_slice(fdg_admm_s* a, int f) {
+  switch (f) {
+    case FDG_F_DIAGJ: return &a->h_diag_j;
+    case FDG_F_DIAGJ2: return &a->h_diag_j2;
+    case FDG_F_M2: return &a->h_m2;
+    case FDG_F_A2INV: return &a->h_a2inv;
+    default: return nullptr;
+  }
+}
+
+void check_ctx(fdg_ctx c) {
+  if (!c) fail(FDG_EINVAL, "fdg: null context");
+  c->set_device();
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+const char* fdg_last_error(void) { return g_err.c_str(); }
+int fdg_last_numeric_code(void) { return g_num; }
+const char* fdg_version(void) { return "fdg 0.1 (sm_100a)"; }
+
+fdg_status fdg_ctx_create(int device, void* stream, fdg_ctx* out) {
+  return guard([&] {
+    int ndev = 0;
+    ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) fail(FDG_EINVAL, "fdg_ctx_create: bad device index");
+    auto c = std::make_unique<fdg_ctx_s>();
+    c->device = device;
+    c->set_device();
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+      c->own_stream = true;
+    }
+    ck(cudaMallocHost(&c->pinned, sizeof(double) * 64), "pinned");
+    c->ensure_partials(4096);
+    *out = c.release();
+  });
+}
+
+fdg_status fdg_ctx_destroy(fdg_ctx ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    ctx->set_device();
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+void* fdg_ctx_stream(fdg_ctx ctx) { return ctx ? ctx->stream : nullptr; }
+uint64_t fdg_ctx_launch_count(fdg_ctx ctx) { return ctx ? ctx->lc.count : 0; }
+fdg_status fdg_ctx_synchronize(fdg_ctx ctx) {
+  return guard([&] {
+    check_ctx(ctx);
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+// --------------------------------------------------------------- setup
+fdg_status fdg_frac_coeffs(double order, int count, double* out) {
+  return guard([&] {
+    const auto g = frac_coeffs_host(order, count);
+    std::memcpy(out, g.data(), sizeof(double) * g.size());
+  });
+}
+
+fdg_status fdg_build_riesz(double beta, int n, double h, double* col, double* row) {
+  return guard([&] {
+    if (!(beta > 1.0 && beta < 2.0)) fail(FDG_EINVAL, "build_riesz: beta must lie in (1, 2)");
+    if (n < 1 || !(h > 0.0)) fail(FDG_EINVAL, "build_riesz: bad grid parameters");
+    const double c = std::cos(beta * 3.14159265358979323846 / 2.0);
+    if (std::abs(c) < 1e-6) fail(FDG_EINVAL, "build_riesz: beta too close to 1");
+    const auto g = frac_coeffs_host(beta, n + 1);
+    const double scale = -1.0 / (2.0 * c * std::pow(h, beta));
+    col[0] = scale * 2.0 * g[1];
+    if (n > 1) col[1] = scale * (g[2] + g[0]);
+    for (int k = 2; k < n; ++k) col[k] = scale * g[k + 1];
+    if (row) std::memcpy(row, col, sizeof(double) * n);
+  });
+}
+
+fdg_status fdg_build_caputo(double alpha, int n, double h, double* col, double* row) {
+  return guard([&] {
+    if (!(alpha > 0.0 && alpha < 1.0)) fail(FDG_EINVAL, "build_caputo: alpha must lie in (0, 1)");
+    if (n < 1 || !(h > 0.0)) fail(FDG_EINVAL, "build_caputo: bad grid parameters");
+    const double scale = 1.0 / std::pow(h, alpha);
+    auto g = frac_coeffs_host(alpha, n);
+    for (int k = 0; k < n; ++k) col[k] = g[k] * scale;
+    for (int k = 0; k < n; ++k) row[k] = 0.0;
+    row[0] = col[0];
+  });
+}
+
+fdg_status fdg_tchan(int n, const double* col, const double* row, double* first_col, double* eigs) {
+  return guard([&] {
+    if (n < 1) fail(FDG_EINVAL, "tchan: empty spec");
+    tchan_host(n, col, row, first_col, eigs);
+  });
+}
+
+fdg_status fdg_randn(uint64_t seed, size_t count, double* out) {
+  return guard([&] {
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> gauss;
+    for (size_t i = 0; i < count; ++i) out[i] = gauss(rng);
+  });
+}
+
+// ------------------------------------------------------------ operator
+fdg_status fdg_op_create(fdg_ctx ctx, int nt, int n1, int n2, const double* tcol, const double* trow,
+                         const double* c1, const double* r1, const double* c2, const double* r2, double psi,
+                         fdg_op* out) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (nt < 1 || n1 < 1 || n2 < 1) fail(FDG_EINVAL, "ConstraintOperator: factor size mismatch");
+    if (!tcol || !trow || !c1 || !r1 || !c2 || !r2) fail(FDG_EINVAL, "fdg_op_create: null factor");
+    auto op = std::make_unique<fdg_op_s>();
+    op->ctx = ctx;
+    op->nt = nt;
+    op->n1 = n1;
+    op->n2 = n2;
+    op->psi = psi;
+    op->tcol.assign(tcol, tcol + nt);
+    op->trow.assign(trow, trow + nt);
+    op->c1.assign(c1, c1 + n1);
+    op->r1.assign(r1, r1 + n1);
+    op->c2.assign(c2, c2 + n2);
+    op->r2.assign(r2, r2 + n2);
+    // As in the reference, the adjoint transposes only the time factor; the
+    // spatial passes use the forward symbols in both directions
+    // (toeplitz.cpp:178-181, "Riesz factors are symmetric").
+    build_axis(op.get(), op->ax1, op->sym1, nullptr, op->tw1, op->c1, op->r1);
+    build_axis(op.get(), op->ax2, op->sym2, nullptr, op->tw2, op->c2, op->r2);
+    bool bidiag = true;
+    for (int k = 1; k < nt; ++k)
+      if (op->trow[k] != 0.0) bidiag = false;
+    for (int k = 2; k < nt; ++k)
+      if (op->tcol[k] != 0.0) bidiag = false;
+    if (bidiag) {
+      op->tf.kind = 1;
+      op->tf.c0 = op->tcol[0];
+      op->tf.c1 = nt > 1 ? op->tcol[1] : 0.0;
+    } else {
+      op->tf.kind = 2;
+      build_axis(op.get(), op->tf.fft, op->symt, &op->symt_adj, op->twt, op->tcol, op->trow);
+    }
+    ctx->ensure_partials(fdg::max_partials_needed(nt, n1, n2));
+    *out = op.release();
+  });
+}
+
+fdg_status fdg_op_destroy(fdg_op op) {
+  return guard([&] {
+    if (op) {
+      op->ctx->set_device();
+      cudaStreamSynchronize(op->ctx->stream);
+    }
+    delete op;
+  });
+}
+
+size_t fdg_op_size(fdg_op op) { return op ? op->N() : 0; }
+double fdg_op_psi(fdg_op op) { return op ? op->psi : 0.0; }
+
+fdg_status fdg_op_apply(fdg_op op, const double* x, double* out, int adjoint) {
+  return guard([&] {
+    if (!op) fail(FDG_EINVAL, "fdg_op_apply: null operator");
+    op->ctx->set_device();
+    if (x == out) fail(FDG_EINVAL, "ConstraintOperator::apply: x and out must not alias");
+    op_apply_dev(op, x, out, adjoint != 0);
+  });
+}
+
+fdg_status fdg_op_apply_host(fdg_op op, const double* x, size_t n_x, double* out, size_t n_out, int adjoint) {
+  return guard([&] {
+    if (!op) fail(FDG_EINVAL, "fdg_op_apply: null operator");
+    if (n_x != op->N() || n_out != op->N())
+      fail(FDG_EINVAL, "ConstraintOperator::apply: dimension mismatch");
+    op->ctx->set_device();
+    cudaStream_t st = op->ctx->stream;
+    DevBuf dx(sizeof(double) * n_x), dout(sizeof(double) * n_out);
+    ck(cudaMemcpyAsync(dx.p, x, sizeof(double) * n_x, cudaMemcpyHostToDevice, st), "H2D");
+    op_apply_dev(op, dx.d(), dout.d(), adjoint != 0);
+    ck(cudaMemcpyAsync(out, dout.p, sizeof(double) * n_out, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+// ------------------------------------------------------ preconditioner
+namespace {
+
+fdg_pc_s* make_pc(fdg_ctx ctx, int nt, int n1, int n2, const double* lt, const double* l1, const double* l2,
+                  double psi, double rho, double delta, double gamma) {
+  if (!(rho > 0.0) || !(delta > 0.0) || !(gamma > 0.0))
+    fail(FDG_EINVAL, "CirculantPreconditioner: scalars must be positive");
+  for (int n : {nt, n1, n2})
+    if (!is_pow2(n) || n > 2048)
+      fail(FDG_EUNSUPPORTED, "fdg: circulant preconditioner needs power-of-two level sizes (got " +
+                                 std::to_string(n) + ")");
+  // The Hartley formulation needs lambda_S even in every axis: real (hence
+  // even) spatial eigenvalues, i.e. symmetric spatial factors.
+  for (auto [lam, n] : {std::pair{l1, n1}, std::pair{l2, n2}}) {
+    double mx = 0.0, im = 0.0;
+    for (int i = 0; i < n; ++i) {
+      mx = std::max(mx, std::hypot(lam[2 * i], lam[2 * i + 1]));
+      im = std::max(im, std::abs(lam[2 * i + 1]));
+    }
+    if (im > 1e-10 * std::max(mx, 1e-300))
+      fail(FDG_EUNSUPPORTED, "fdg: spatial circulant eigenvalues must be real (symmetric factors)");
+  }
+  auto pc = std::make_unique<fdg_pc_s>();
+  pc->ctx = ctx;
+  pc->nt = nt;
+  pc->n1 = n1;
+  pc->n2 = n2;
+  pc->psi = psi;
+  pc->rho = rho;
+  pc->delta = delta;
+  pc->gamma = gamma;
+  cudaStream_t st = ctx->stream;
+  upload(pc->lt, std::vector<double>(lt, lt + 2 * (size_t)nt), st);
+  upload(pc->l1, std::vector<double>(l1, l1 + 2 * (size_t)n1), st);
+  upload(pc->l2, std::vector<double>(l2, l2 + 2 * (size_t)n2), st);
+  upload(pc->twt, twiddles(nt), st);
+  upload(pc->tw1, twiddles(n1), st);
+  upload(pc->tw2, twiddles(n2), st);
+  // circulant.cpp:37-40
+  const double m2 = 1.0 / (rho * (gamma / (psi * psi) + 1.0 / delta)) + delta / rho;
+  PcTables& t = pc->tab;
+  t.nt = nt;
+  t.n1 = n1;
+  t.n2 = n2;
+  t.lam_t = pc->lt.c();
+  t.lam_1 = pc->l1.c();
+  t.lam_2 = pc->l2.c();
+  t.tw_t = pc->twt.c();
+  t.tw_1 = pc->tw1.c();
+  t.tw_2 = pc->tw2.c();
+  t.psi = psi;
+  t.base = rho * (1.0 + 1.0 / delta);
+  t.inv_m2 = 1.0 / m2;
+  t.inv_total = 1.0 / (double)pc->N();
+  ctx->ensure_partials(fdg::max_partials_needed(nt, n1, n2));
+  return pc.release();
+}
+
+}  // namespace
+
+fdg_status fdg_pc_create(fdg_ctx ctx, int nt, int n1, int n2, const double* lt, const double* l1, const double* l2,
+                         double psi, double rho, double delta, double gamma, fdg_pc* out) {
+  return guard([&] {
+    check_ctx(ctx);
+    *out = make_pc(ctx, nt, n1, n2, lt, l1, l2, psi, rho, delta, gamma);
+  });
+}
+
+fdg_status fdg_pc_assemble(fdg_op op, double rho, double delta, double gamma, fdg_pc* out) {
+  return guard([&] {
+    if (!op) fail(FDG_EINVAL, "assemble_precond: null operator");
+    check_ctx(op->ctx);
+    std::vector<double> lt(2 * (size_t)op->nt), l1(2 * (size_t)op->n1), l2(2 * (size_t)op->n2);
+    tchan_host(op->nt, op->tcol.data(), op->trow.data(), nullptr, lt.data());
+    tchan_host(op->n1, op->c1.data(), op->r1.data(), nullptr, l1.data());
+    tchan_host(op->n2, op->c2.data(), op->r2.data(), nullptr, l2.data());
+    *out = make_pc(op->ctx, op->nt, op->n1, op->n2, lt.data(), l1.data(), l2.data(), op->psi, rho, delta, gamma);
+  });
+}
+
+fdg_status fdg_pc_destroy(fdg_pc pc) {
+  return guard([&] {
+    if (pc) {
+      pc->ctx->set_device();
+      cudaStreamSynchronize(pc->ctx->stream);
+    }
+    delete pc;
+  });
+}
+
+fdg_status fdg_pc_solve(fdg_pc pc, const double* r, double* z) {
+  return guard([&] {
+    if (!pc) fail(FDG_EINVAL, "precond_solve: null preconditioner");
+    pc->ctx->set_device();
+    if (r == z) fail(FDG_EINVAL, "precond_solve: r and z must not alias");
+    pc_apply_dev(pc, r, z, z, nullptr, RedSlot{});
+  });
+}
+
+fdg_status fdg_pc_solve_host(fdg_pc pc, const double* r, size_t n_r, double* z, size_t n_z) {
+  return guard([&] {
+    if (!pc) fail(FDG_EINVAL, "precond_solve: null preconditioner");
+    if (n_r != pc->N() || n_z != pc->N()) fail(FDG_EINVAL, "precond_solve: dimension mismatch");
+    pc->ctx->set_device();
+    cudaStream_t st = pc->ctx->stream;
+    DevBuf dr(sizeof(double) * n_r), dz(sizeof(double) * n_z);
+    ck(cudaMemcpyAsync(dr.p, r, sizeof(double) * n_r, cudaMemcpyHostToDevice, st), "H2D");
+    pc_apply_dev(pc, dr.d(), dz.d(), dz.d(), nullptr, RedSlot{});
+    ck(cudaMemcpyAsync(z, dz.p, sizeof(double) * n_z, cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+fdg_status fdg_pc_lam_s_host(fdg_pc pc, double* out) {
+  return guard([&] {
+    if (!pc) fail(FDG_EINVAL, "null preconditioner");
+    std::vector<double> lt(2 * (size_t)pc->nt), l1(2 * (size_t)pc->n1), l2(2 * (size_t)pc->n2);
+    pc->ctx->set_device();
+    ck(cudaMemcpy(lt.data(), pc->lt.p, lt.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(l1.data(), pc->l1.p, l1.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(l2.data(), pc->l2.p, l2.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+    const double m2 = 1.0 / pc->tab.inv_m2;
+    for (int k = 0; k < pc->nt; ++k)
+      for (int i = 0; i < pc->n1; ++i)
+        for (int j = 0; j < pc->n2; ++j) {
+          const double sr = l1[2 * i] + l2[2 * j], si = l1[2 * i + 1] + l2[2 * j + 1];
+          const double br = pc->psi * (lt[2 * k] - sr), bi = pc->psi * (lt[2 * k + 1] - si);
+          out[((size_t)k * pc->n1 + i) * pc->n2 + j] = pc->tab.base + (br * br + bi * bi) / m2;
+        }
+  });
+}
+
+// ---------------------------------------------------------------- ADMM
+fdg_status fdg_admm_create(fdg_op op, fdg_pc pc, const fdg_admm_desc* desc, const double* ybar, fdg_admm* out) {
+  return guard([&] {
+    if (!op || !pc || !desc) fail(FDG_EINVAL, "fdg_admm_create: null argument");
+    if (op->ctx != pc->ctx) fail(FDG_EINVAL, "fdg_admm_create: operator and preconditioner on different contexts");
+    if (op->nt != pc->nt || op->n1 != pc->n1 || op->n2 != pc->n2)
+      fail(FDG_EINVAL, "fdg_admm_create: operator/preconditioner shape mismatch");
+    const fdg_admm_desc& d = *desc;
+    // AdmmConfig::validate (admm.cpp:34-42) and ProblemSpec::validate bounds/gamma
+    constexpr double rho_max = 1.6180339887498949;
+    if (!(d.rho > 0.0 && d.rho < rho_max)) fail(FDG_EINVAL, "rho must lie in (0, (sqrt(5)+1)/2)");
+    if (!(d.delta > 0.0)) fail(FDG_EINVAL, "delta must be positive");
+    if (!(d.tol_primal > 0.0) || !(d.inner_tol_floor > 0.0) || !(d.inner_tol_factor > 0.0))
+      fail(FDG_EINVAL, "tolerances must be positive");
+    if (d.max_outer < 1 || d.max_inner < 1) fail(FDG_EINVAL, "iteration caps must be >= 1");
+    if (!(d.gamma > 0.0)) fail(FDG_EINVAL, "gamma must be positive");
+    if (!(d.y_lo < d.y_hi)) fail(FDG_EINVAL, "state bounds must satisfy y_lo < y_hi");
+    if (!(d.u_lo < d.u_hi)) fail(FDG_EINVAL, "control bounds must satisfy u_lo < u_hi");
+    fdg_ctx ctx = op->ctx;
+    check_ctx(ctx);
+    auto a = std::make_unique<fdg_admm_s>();
+    a->op = op;
+    a->pc = pc;
+    a->desc = d;
+    a->nt = op->nt;
+    a->slice = (size_t)op->n1 * op->n2;
+    a->N = op->N();
+    a->psi = op->psi;
+    a->v_lo = a->psi * d.u_lo;
+    a->v_hi = a->psi * d.u_hi;
+    const int nt = op->nt;
+    // make_admm_work (admm.cpp:52-79) + objective_weights (problem.cpp:60-68)
+    a->h_diag_j.assign(nt, 1.0);
+    a->h_diag_j[nt - 1] = 0.5;
+    a->h_diag_j2.resize(nt);
+    a->h_m2.resize(nt);
+    a->h_a2inv.resize(nt);
+    std::vector<double> inv_m2(nt), a1(nt);
+    const double g_over_psi2 = d.gamma / (a->psi * a->psi);
+    for (int k = 0; k < nt; ++k) {
+      a->h_diag_j2[k] = g_over_psi2 * a->h_diag_j[k];
+      a->h_a2inv[k] = 1.0 / (d.rho * (a->h_diag_j2[k] + 1.0 / d.delta));
+      a->h_m2[k] = a->h_a2inv[k] + d.delta / d.rho;
+      inv_m2[k] = 1.0 / a->h_m2[k];
+      a1[k] = d.rho * (a->h_diag_j[k] + 1.0 / d.delta);
+    }
+    cudaStream_t st = ctx->stream;
+    upload(a->diag_j, a->h_diag_j, st);
+    upload(a->diag_j2, a->h_diag_j2, st);
+    upload(a->m2, a->h_m2, st);
+    upload(a->a2inv, a->h_a2inv, st);
+    upload(a->inv_m2, inv_m2, st);
+    upload(a->a1, a1, st);
+    const size_t bytes = sizeof(double) * a->N;
+    for (DevBuf* b : {&a->y, &a->v, &a->z_y, &a->z_v, &a->p, &a->w_y, &a->w_v, &a->ybar, &a->By, &a->rhs, &a->r_cache,
+                      &a->tmp, &a->r, &a->z, &a->d, &a->u, &a->w, &a->vp}) {
+      b->alloc(bytes);
+      ck(cudaMemsetAsync(b->p, 0, bytes, st), "memset");
+    }
+    if (ybar) ck(cudaMemcpyAsync(a->ybar.p, ybar, bytes, cudaMemcpyHostToDevice, st), "ybar H2D");
+    a->sc.init(ctx);
+    a->inner_tol = d.inner_tol_factor * d.inner_tol_floor;  // admm.cpp:245
+    for (cudaEvent_t* e : {&a->e0, &a->e1, &a->e2, &a->e3}) ck(cudaEventCreate(e), "event");
+    ck(cudaStreamSynchronize(st), "sync");
+    *out = a.release();
+  });
+}
+
+fdg_status fdg_admm_destroy(fdg_admm a) {
+  return guard([&] {
+    if (!a) return;
+    a->op->ctx->set_device();
+    cudaStreamSynchronize(a->op->ctx->stream);
+    for (cudaEvent_t e : {a->e0, a->e1, a->e2, a->e3})
+      if (e) cudaEventDestroy(e);
+    delete a;
+  });
+}
+
+int fdg_admm_converged(fdg_admm a) { return a && a->converged ? 1 : 0; }
+int fdg_admm_stagnations(fdg_admm a) { return a ? a->stagnations : 0; }
+
+fdg_status fdg_admm_get(fdg_admm a, int field, double* out) {
+  return guard([&] {
+    if (!a) fail(FDG_EINVAL, "null admm");
+    a->op->ctx->set_device();
+    if (double* p = field_dev(a, field)) {
+      ck(cudaMemcpyAsync(out, p, sizeof(double) * a->N, cudaMemcpyDeviceToHost, a->op->ctx->stream), "D2H");
+      ck(cudaStreamSynchronize(a->op->ctx->stream), "sync");
+      return;
+    }
+    const auto* s = field_slice(a, field);
+    if (!s) fail(FDG_EINVAL, "fdg_admm_get: unknown field");
+    for (size_t i = 0; i < a->N; ++i) out[i] = (*s)[i / a->slice];
+  });
+}
+
+fdg_status fdg_admm_set(fdg_admm a, int field, const double* in) {
+  return guard([&] {
+    if (!a) fail(FDG_EINVAL, "null admm");
+    a->op->ctx->set_device();
+    double* p = field_dev(a, field);
+    if (!p) fail(FDG_EINVAL, "fdg_admm_set: field is not settable");
+    ck(cudaMemcpyAsync(p, in, sizeof(double) * a->N, cudaMemcpyHostToDevice, a->op->ctx->stream), "H2D");
+    ck(cudaStreamSynchronize(a->op->ctx->stream), "sync");
+  });
+}
+
+fdg_status fdg_admm_field_ptr(fdg_admm a, int field, double** dev) {
+  return guard([&] {
+    if (!a) fail(FDG_EINVAL, "null admm");
+    double* p = field_dev(a, field);
+    if (!p) fail(FDG_EINVAL, "fdg_admm_field_ptr: unknown field");
+    *dev = p;
+  });
+}
+
+fdg_status fdg_admm_apply_S(fdg_admm a, const double* x, double* out) {
+  return guard([&] {
+    if (!a) fail(FDG_EINVAL, "null admm");
+    a->op->ctx->set_device();
+    apply_S_dev(a, x, out);
+  });
+}
+
+fdg_status fdg_admm_build_rhs(fdg_admm a, double* rhs, double* r_cache) {
+  return guard([&] {
+    if (!a) fail(FDG_EINVAL, "null admm");
+    a->op->ctx->set_device();
+    build_rhs_dev(a, rhs, r_cache ? r_cache : a->r_cache.d());
+  });
+}
+
+fdg_status fdg_admm_pcg(fdg_admm a, const double* rhs, double* x, double tol, int max_inner, fdg_pcg_result* res) {
+  return guard([&] {
+    if (!a) fail(FDG_EINVAL, "null admm");
+    a->op->ctx->set_device();
+    const fdg_pcg_result r = pcg_dev(a, rhs, x, tol, max_inner);
+    if (res) *res = r;
+  });
+}
+
+fdg_status fdg_admm_pcg_host(fdg_admm a, const double* rhs, double* x, double tol, int max_inner,
+                             fdg_pcg_result* res) {
+  return guard([&] {
+    if (!a) fail(FDG_EINVAL, "null admm");
+    a->op->ctx->set_device();
+    cudaStream_t st = a->op->ctx->stream;
+    const size_t bytes = sizeof(double) * a->N;
+    ck(cudaMemcpyAsync(a->rhs.p, rhs, bytes, cudaMemcpyHostToDevice, st), "H2D rhs");
+    ck(cudaMemcpyAsync(a->tmp.p, x, bytes, cudaMemcpyHostToDevice, st), "H2D x");
+    const fdg_pcg_result r = pcg_dev(a, a->rhs.d(), a->tmp.d(), tol, max_inner);
+    ck(cudaMemcpyAsync(x, a->tmp.p, bytes, cudaMemcpyDeviceToHost, st), "D2H x");
+    ck(cudaStreamSynchronize(st), "sync");
+    if (res) *res = r;
+  });
+}
+
+fdg_status fdg_admm_dual_inf(fdg_admm a, double* out) {
+  return guard([&] {
+    if (!a) fail(FDG_EINVAL, "null admm");
+    a->op->ctx->set_device();
+    cudaStream_t st = a->op->ctx->stream;
+    op_apply_dev(a->op, a->p.d(), a->tmp.d(), true);
+    ck(fdg::launch_dual_inf(st, &a->op->ctx->lc, a->y.d(), a->ybar.d(), a->tmp.d(), a->w_y.d(), a->v.d(), a->p.d(),
+                            a->w_v.d(), a->diag_j.d(), a->diag_j2.d(), a->slice, a->N, a->sc.slot(S_DINF)),
+       "dual inf");
+    double s[2];
+    a->sc.read(S_DINF, 2, s);
+    *out = std::max(s[0], s[1]);
+  });
+}
+
+fdg_status fdg_admm_objective(fdg_admm a, double* out) {
+  return guard([&] {
+    if (!a) fail(FDG_EINVAL, "null admm");
+    a->op->ctx->set_device();
+    ck(fdg::launch_objective(a->op->ctx->stream, &a->op->ctx->lc, a->y.d(), a->ybar.d(), a->v.d(), a->diag_j.d(),
+                             a->diag_j2.d(), a->slice, a->N, a->sc.slot(S_OBJ)),
+       "objective");
+    double s[2];
+    a->sc.read(S_OBJ, 2, s);
+    *out = 0.5 * s[0] + 0.5 * s[1];
+  });
+}
+
+// AdmmDriver::step (admm.cpp:245-277)
+fdg_status fdg_admm_step(fdg_admm a, fdg_iter_record* rec) {
+  return guard([&] {
+    if (!a) fail(FDG_EINVAL, "null admm");
+    fdg_ctx ctx = a->op->ctx;
+    ctx->set_device();
+    cudaStream_t st = ctx->stream;
+    LaunchCounter* lc = &ctx->lc;
+    const auto& d = a->desc;
+    ck(cudaEventRecord(a->e2, st), "event");
+    build_rhs_dev(a, a->rhs.d(), a->r_cache.d());
+    if (!d.warm_start) ck(fdg::launch_fill(st, lc, a->y.d(), 0.0, a->N), "y = 0");
+    const double tol = d.fixed_krylov_tol > 0.0 ? d.fixed_krylov_tol : a->inner_tol;
+    const fdg_pcg_result inner = pcg_dev(a, a->rhs.d(), a->y.d(), tol, d.max_inner);
+    a->stagnations = inner.converged ? 0 : a->stagnations + 1;
+    op_apply_dev(a->op, a->y.d(), a->By.d(), false);
+    ck(fdg::launch_admm_update(st, lc, admm_scalars(a), a->y.d(), a->v.d(), a->z_y.d(), a->z_v.d(), a->p.d(),
+                               a->w_y.d(), a->w_v.d(), a->By.d(), a->r_cache.d(), a->a2inv.d(), a->m2.d(), a->slice,
+                               a->N, a->sc.slot(S_ADMM)),
+       "admm update");
+    ++a->iteration;
+    // dual_infeasibility (admm.cpp:275)
+    op_apply_dev(a->op, a->p.d(), a->tmp.d(), true);
+    ck(fdg::launch_dual_inf(st, lc, a->y.d(), a->ybar.d(), a->tmp.d(), a->w_y.d(), a->v.d(), a->p.d(), a->w_v.d(),
+                            a->diag_j.d(), a->diag_j2.d(), a->slice, a->N, a->sc.slot(S_DINF)),
+       "dual inf");
+    ck(cudaEventRecord(a->e3, st), "event");
+    double s[6];
+    a->sc.read(S_ADMM, 6, s);  // r_eq, r_y, r_v, bad, s1, s2
+    if (s[3] != 0.0)
+      fail(FDG_ENUMERIC, "admm: non-finite iterate at outer iteration " + std::to_string(a->iteration),
+           FDG_NUM_NONFINITE_ITERATE);
+    const double r_eq = s[0], r_y = s[1], r_u = s[2] / a->psi;
+    const double tolp = d.tol_primal;
+    a->converged = (r_eq <= tolp && r_y <= tolp && r_u <= tolp);
+    a->inner_tol = d.inner_tol_factor * std::max(std::min({r_eq, r_y, r_u}), d.inner_tol_floor);
+    float step_ms = 0.f;
+    ck(cudaEventElapsedTime(&step_ms, a->e2, a->e3), "elapsed");
+    if (rec) {
+      rec->iter = a->iteration;
+      rec->r_eq = r_eq;
+      rec->r_y = r_y;
+      rec->r_u = r_u;
+      rec->dual_inf = std::max(s[4], s[5]);
+      rec->inner_iters = inner.iterations;
+      rec->inner_tol = a->inner_tol;
+      rec->converged = a->converged ? 1 : 0;
+      rec->pcg_converged = inner.converged;
+      rec->pcg_rel_residual = inner.rel_residual;
+      rec->pcg_ms = inner.ms;
+      rec->step_ms = step_ms;
+    }
+  });
+}
+
+}  // extern "C"

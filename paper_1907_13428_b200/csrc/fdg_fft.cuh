@@ -1,0 +1,225 @@
+// fdg_fft.cuh — fp64 shared-memory Stockham FFT building blocks for sm_100a.
+//
+// Replaces the arithmetic of fft::BatchedRealFft / fft::Fft3D
+// (/root/reference/proj/src/fft.cpp:25-109, FFTW r2c/c2r/3-D) on the device.
+//
+// Execution model ("lane-interleaved tile"):
+//   * a CTA runs G independent complex FFTs of length N ("lanes");
+//   * lane g uses T = N/R threads; thread (g, t) lives at tid = t*G + g, so a
+//     warp covers 32/G consecutive t of all G lanes;
+//   * thread t of a lane holds x[t + m*T] (m < R) in registers, both at the
+//     input and at the output of the transform (Stockham autosort keeps
+//     natural order on both sides), so pointwise work (symbol multiply,
+//     spectral division) happens in registers between a forward and an
+//     inverse transform with no extra exchange;
+//   * between radix passes the data goes through shared memory laid out as
+//     sm[pos][G] double2: a warp touches 32/G positions x G lanes, i.e. whole
+//     128-byte rows of 8 complex values for G = 8, so exchanges are free of
+//     bank conflicts whatever the Stockham scatter pattern is.
+// Twiddles come from a per-length table W_N[k] = exp(-2 pi i k/N) in global
+// memory (L1-resident), computed on the host in long double.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace fdg {
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+
+// Multiply by W_R^q = exp(-/+ 2 pi i q / R) for compile-time (R, q).
+template <int R, int Q, bool INV>
+__device__ __forceinline__ double2 mul_wq(double2 x) {
+  constexpr int q = ((Q % R) + R) % R;
+  if constexpr (q == 0) {
+    return x;
+  } else if constexpr (4 * q == R) {  // -i (fwd) / +i (inv)
+    return INV ? make_double2(-x.y, x.x) : make_double2(x.y, -x.x);
+  } else if constexpr (2 * q == R) {
+    return make_double2(-x.x, -x.y);
+  } else if constexpr (4 * q == 3 * R) {  // +i (fwd) / -i (inv)
+    return INV ? make_double2(x.y, -x.x) : make_double2(-x.y, x.x);
+  } else if constexpr (8 * q == R || 8 * q == 3 * R || 8 * q == 5 * R || 8 * q == 7 * R) {
+    constexpr double h = 0.70710678118654752440;
+    // cos(2 pi q/R), -sin(2 pi q/R) for q/R in {1/8, 3/8, 5/8, 7/8}
+    constexpr double c = (8 * q == R || 8 * q == 7 * R) ? h : -h;
+    constexpr double s = (8 * q == R || 8 * q == 3 * R) ? -h : h;  // -sin
+    constexpr double si = INV ? -s : s;
+    return make_double2(c * x.x - si * x.y, c * x.y + si * x.x);
+  } else {
+    static_assert(R == 16, "general twiddle constants only for R = 16");
+    constexpr double C1 = 0.92387953251128675613, S1 = 0.38268343236508977173;
+    // q in {1,3,5,7,9,11,13,15}: cos/sin of 2 pi q/16
+    constexpr double cs[16] = {1, C1, 0, S1, 0, -S1, 0, -C1, 0, -C1, 0, -S1, 0, S1, 0, C1};
+    constexpr double sn[16] = {0, S1, 0, C1, 0, C1, 0, S1, 0, -S1, 0, -C1, 0, -C1, 0, -S1};
+    constexpr double c = cs[q];
+    constexpr double s = INV ? sn[q] : -sn[q];
+    return make_double2(c * x.x - s * x.y, c * x.y + s * x.x);
+  }
+}
+
+// In-register DFT of size R (natural order in and out): X_q = sum_r v_r W_R^{rq}.
+template <int R, bool INV>
+struct Dft;
+
+template <bool INV>
+struct Dft<1, INV> {
+  template <class A>
+  __device__ __forceinline__ static void run(A& v, int base, int stride) {}
+};
+
+template <bool INV>
+struct Dft<2, INV> {
+  template <class A>
+  __device__ __forceinline__ static void run(A& v, int base, int stride) {
+    const double2 a = v[base], b = v[base + stride];
+    v[base] = cadd(a, b);
+    v[base + stride] = csub(a, b);
+  }
+};
+
+template <bool INV>
+struct Dft<4, INV> {
+  template <class A>
+  __device__ __forceinline__ static void run(A& v, int base, int stride) {
+    const double2 a = v[base], b = v[base + stride], c = v[base + 2 * stride], d = v[base + 3 * stride];
+    const double2 s0 = cadd(a, c), s1 = csub(a, c), s2 = cadd(b, d), s3 = mul_wq<4, 1, INV>(csub(b, d));
+    v[base] = cadd(s0, s2);
+    v[base + 2 * stride] = csub(s0, s2);
+    v[base + stride] = cadd(s1, s3);
+    v[base + 3 * stride] = csub(s1, s3);
+  }
+};
+
+// Radix-2 decimation in time on top of two half-size DFTs (R = 8, 16).
+template <int R, bool INV>
+struct Dft {
+  static_assert(R == 8 || R == 16, "unsupported radix");
+  template <class A>
+  __device__ __forceinline__ static void run(A& v, int base, int stride) {
+    constexpr int H = R / 2;
+    double2 e[H], o[H];
+#pragma unroll
+    for (int r = 0; r < H; ++r) {
+      e[r] = v[base + (2 * r) * stride];
+      o[r] = v[base + (2 * r + 1) * stride];
+    }
+    Dft<H, INV>::run(e, 0, 1);
+    Dft<H, INV>::run(o, 0, 1);
+    combine<0>(v, base, stride, e, o);
+  }
+  template <int Q, class A>
+  __device__ __forceinline__ static void combine(A& v, int base, int stride, const double2 (&e)[R / 2],
+                                                 const double2 (&o)[R / 2]) {
+    if constexpr (Q < R / 2) {
+      const double2 t = mul_wq<R, Q, INV>(o[Q]);
+      v[base + Q * stride] = cadd(e[Q], t);
+      v[base + (Q + R / 2) * stride] = csub(e[Q], t);
+      combine<Q + 1>(v, base, stride, e, o);
+    }
+  }
+};
+
+// Compile-time radix plan: passes of radix min(R, N/Ns).
+template <int N, int R, int Ns>
+struct PassRadix {
+  static constexpr int value = (N / Ns) < R ? (N / Ns) : R;
+};
+
+// One Stockham pass on a lane (registers in, registers out, with the
+// shared-memory scatter of the pass output unless it is the last pass).
+//   N   : transform length, R: registers per thread, T = N/R
+//   Ns  : product of previous radices
+//   G   : lanes per CTA (smem row width)
+template <int N, int R, int G, bool INV, int Ns>
+struct Stockham {
+  static constexpr int T = N / R;
+  static constexpr int Rp = PassRadix<N, R, Ns>::value;
+  static constexpr int S = R / Rp;  // butterflies per thread in this pass
+  static constexpr bool LAST = (Ns * Rp == N);
+
+  __device__ __forceinline__ static void run(double2 (&v)[R], double2* sm, int t, int g,
+                                             const double2* __restrict__ tw) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int b = t + s * T;  // butterfly index in [0, N/Rp)
+      if constexpr (Ns > 1) {
+        const int bm = b % Ns;
+#pragma unroll
+        for (int r = 1; r < Rp; ++r) {
+          const double2 w = __ldg(&tw[bm * r * (N / (Ns * Rp))]);
+          v[s + r * S] = INV ? cmulc(v[s + r * S], w) : cmul(v[s + r * S], w);
+        }
+      }
+      Dft<Rp, INV>::run(v, s, S);
+    }
+    if constexpr (!LAST) {
+      // scatter: out[(b/Ns)*Ns*Rp + b%Ns + r*Ns] = v[s + r*S]
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int b = t + s * T;
+        const int base = (b / Ns) * Ns * Rp + (b % Ns);
+#pragma unroll
+        for (int r = 0; r < Rp; ++r) sm[(base + r * Ns) * G + g] = v[s + r * S];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int m = 0; m < R; ++m) v[m] = sm[(t + m * T) * G + g];
+      __syncthreads();
+      Stockham<N, R, G, INV, Ns * Rp>::run(v, sm, t, g, tw);
+    }
+  }
+};
+
+// Terminal specialization guard (never instantiated with Ns >= N).
+template <int N, int R, int G, bool INV>
+struct StockhamEnd {
+  __device__ __forceinline__ static void run(double2 (&)[R], double2*, int, int, const double2*) {}
+};
+
+// Full FFT of length N on the lane; x[t + m*T] in v[m] before and after.
+// Every thread of the CTA must call it (it contains __syncthreads()).
+template <int N, int R, int G, bool INV>
+__device__ __forceinline__ void fft_lane(double2 (&v)[R], double2* sm, int t, int g,
+                                         const double2* __restrict__ tw) {
+  if constexpr (N == 1) {
+    return;
+  } else {
+    Stockham<N, R, G, INV, 1>::run(v, sm, t, g, tw);
+  }
+}
+
+// Exchange helper: value at position (N - pos) mod N for every register
+// (used by the Hartley post-processing).  Contains two __syncthreads().
+template <int N, int R, int G>
+__device__ __forceinline__ void mirror_lane(const double2 (&v)[R], double2 (&w)[R], double2* sm, int t,
+                                            int g) {
+  constexpr int T = N / R;
+#pragma unroll
+  for (int m = 0; m < R; ++m) sm[(t + m * T) * G + g] = v[m];
+  __syncthreads();
+#pragma unroll
+  for (int m = 0; m < R; ++m) {
+    const int pos = t + m * T;
+    const int mp = pos == 0 ? 0 : N - pos;
+    w[m] = sm[mp * G + g];
+  }
+  __syncthreads();
+}
+
+// Two packed real sequences a + i b -> (Hartley(a), Hartley(b)) given
+// Z = FFT(a + i b): H_a[f] = (zr - zi + wr + wi)/2, H_b[f] = (zr + zi - wr + wi)/2
+// with W = Z[N - f].  Returned packed as H_a + i H_b.
+__device__ __forceinline__ double2 hartley_split(double2 z, double2 w) {
+  return make_double2(0.5 * ((z.x - z.y) + (w.x + w.y)), 0.5 * ((z.x + z.y) - (w.x - w.y)));
+}
+
+}  // namespace fdg

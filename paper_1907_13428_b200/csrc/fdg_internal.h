@@ -1,0 +1,137 @@
+// fdg_internal.h — host-side declarations shared by the C-ABI layer and the
+// kernel launchers.  Not part of the public interface (include/fdg.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "fdg_reduce.cuh"
+
+namespace fdg {
+
+// Device-resident description of one spatial/temporal Toeplitz factor used by
+// the FFT passes: the full length-L circulant-embedding symbol (L pow2 >=
+// 2n-1) and the matching twiddle table, both double2[L].
+struct AxisSym {
+  int n = 0;  // factor size
+  int L = 0;  // embedding length (power of two)
+  const double2* sym = nullptr;      // forward factor symbol
+  const double2* sym_adj = nullptr;  // transposed factor symbol (== sym if symmetric)
+  const double2* tw = nullptr;       // W_L twiddles
+};
+
+// Time coupling.  kind 0: no time term; 1: lower-bidiagonal stencil
+// (c0 x_k + c1 x_{k-1}; adjoint c0 x_k + c1 x_{k+1}); 2: general Toeplitz
+// applied by an FFT pass along t.
+struct TimeFactor {
+  int kind = 0;
+  double c0 = 0.0, c1 = 0.0;  // unscaled stencil coefficients
+  AxisSym fft;                // kind 2
+};
+
+// Per-launch bookkeeping (kernel count for the bench's gpu_launches claim).
+struct LaunchCounter {
+  unsigned long long count = 0;
+};
+
+// Spectral tables of the circulant preconditioner (1-D eigenvalues, complex).
+struct PcTables {
+  int nt = 0, n1 = 0, n2 = 0;
+  const double2* lam_t = nullptr;
+  const double2* lam_1 = nullptr;
+  const double2* lam_2 = nullptr;
+  const double2* tw_t = nullptr;  // W_nt
+  const double2* tw_1 = nullptr;  // W_n1
+  const double2* tw_2 = nullptr;  // W_n2
+  double psi = 1.0, base = 0.0, inv_m2 = 0.0, inv_total = 0.0;
+};
+
+// ---------------------------------------------------------------- launchers
+// All return cudaGetLastError() of the launch.  `lc` may be null.
+
+// out = time(x) - psi * L2 x along x2 (rows), with time handled here when it
+// is a stencil (kind 1).  adjoint selects the transposed time stencil.
+cudaError_t launch_row_apply(cudaStream_t st, LaunchCounter* lc, const double* x, double* out, int nt,
+                             int n1, int n2, const AxisSym& s2, double scale, const TimeFactor& tf,
+                             double psi, bool adjoint);
+
+// out = acc + scale * T(x) along an axis of length n with inner count C and
+// outer count O (axis x1: O = nt, C = n2; axis t: O = 1, C = n1*n2).
+cudaError_t launch_col_acc(cudaStream_t st, LaunchCounter* lc, const double* x, const double* acc,
+                           double* out, int O, int n, int C, const AxisSym& s, double scale,
+                           bool adjoint);
+
+// Fused S pass 2 (x1 columns): Bp = u + scale*L1 p; w = Bp/m2[k];
+// vp = scale*L1 w + a1[k] p; reduces sum(a1 p^2 + w Bp) = p^T S p.
+cudaError_t launch_col_s_mid(cudaStream_t st, LaunchCounter* lc, const double* p, const double* u,
+                             double* w, double* vp, int nt, int n1, int n2, const AxisSym& s1,
+                             double scale, const double* inv_m2, const double* a1, RedSlot red);
+
+// Fused S pass 3 (x2 rows) + residual update: q = vp + time^T(w) + scale*L2 w;
+// if q_out: q_out = q; if r: r -= alpha q with alpha = *num / *den, reduce |r|^2.
+cudaError_t launch_row_s_out(cudaStream_t st, LaunchCounter* lc, const double* w, const double* vp,
+                             double* q_out, double* r, int nt, int n1, int n2, const AxisSym& s2,
+                             double scale, const TimeFactor& tf, double psi, const double* alpha_num,
+                             const double* alpha_den, RedSlot red);
+
+// Preconditioner passes (pow2 lengths).
+cudaError_t launch_hartley_row(cudaStream_t st, LaunchCounter* lc, const double* in, double* out, int F,
+                               int n, const double2* tw, const double* rdot, RedSlot red);
+cudaError_t launch_hartley_col(cudaStream_t st, LaunchCounter* lc, double* data, int O, int n, int C,
+                               const double2* tw);
+cudaError_t launch_t_filter(cudaStream_t st, LaunchCounter* lc, double* data, const PcTables& pt);
+
+// ------------------------------------------------------------- elementwise
+cudaError_t launch_copy(cudaStream_t st, LaunchCounter* lc, double* dst, const double* src, size_t N);
+cudaError_t launch_fill(cudaStream_t st, LaunchCounter* lc, double* dst, double v, size_t N);
+// sum of squares (or dot when b != null) -> red.result[0]
+cudaError_t launch_dot(cudaStream_t st, LaunchCounter* lc, const double* a, const double* b, size_t N,
+                       RedSlot red);
+// x += alpha p (alpha = num/den, optional), p = z + beta p (beta = bnum/bden)
+cudaError_t launch_cg_update(cudaStream_t st, LaunchCounter* lc, double* x, double* p, const double* z,
+                             size_t N, const double* a_num, const double* a_den, const double* b_num,
+                             const double* b_den, bool update_x);
+// x += alpha p only
+cudaError_t launch_axpy_dev(cudaStream_t st, LaunchCounter* lc, double* x, const double* p, size_t N,
+                            const double* a_num, const double* a_den);
+// r = b - q, reduce |r|^2
+cudaError_t launch_residual(cudaStream_t st, LaunchCounter* lc, double* r, const double* b,
+                            const double* q, size_t N, RedSlot red);
+// out = a1[k] x (S with B == 0 part), used by the generic apply_S path
+cudaError_t launch_scale_by_slice(cudaStream_t st, LaunchCounter* lc, double* out, const double* x,
+                                  const double* coef, size_t slice, size_t N);
+
+// ADMM elementwise stages (admm.cpp:100-119, 171-233) -- see fdg_kernels.cu.
+struct AdmmScalars {
+  double rho, delta, psi;
+  double y_lo, y_hi, v_lo, v_hi;
+};
+cudaError_t launch_rhs_pre(cudaStream_t st, LaunchCounter* lc, const AdmmScalars& a, const double* p,
+                           const double* w_v, const double* z_v, const double* a2inv,
+                           const double* m2, double* r_cache, double* tmp, size_t slice, size_t N);
+cudaError_t launch_rhs_post(cudaStream_t st, LaunchCounter* lc, const AdmmScalars& a, double* rhs,
+                            const double* ybar, const double* w_y, const double* z_y,
+                            const double* diag_j, size_t slice, size_t N);
+// Fused recover_vp + z_update + dual_update + check_termination maxima + finiteness.
+// red.result = {r_eq, r_y, r_v, nonfinite_flag}
+cudaError_t launch_admm_update(cudaStream_t st, LaunchCounter* lc, const AdmmScalars& a, const double* y,
+                               double* v, double* z_y, double* z_v, double* p, double* w_y,
+                               double* w_v, const double* By, const double* r_cache,
+                               const double* a2inv, const double* m2, size_t slice, size_t N,
+                               RedSlot red);
+// dual infeasibility maxima {s1, s2}
+cudaError_t launch_dual_inf(cudaStream_t st, LaunchCounter* lc, const double* y, const double* ybar,
+                            const double* btp, const double* w_y, const double* v, const double* p,
+                            const double* w_v, const double* diag_j, const double* diag_j2,
+                            size_t slice, size_t N, RedSlot red);
+// objective {sum J (y - ybar)^2, sum J2 v^2}
+cudaError_t launch_objective(cudaStream_t st, LaunchCounter* lc, const double* y, const double* ybar,
+                             const double* v, const double* diag_j, const double* diag_j2,
+                             size_t slice, size_t N, RedSlot red);
+
+// Grid of the reduction-bearing kernels (to size partial buffers).
+size_t max_partials_needed(int nt, int n1, int n2);
+
+}  // namespace fdg
