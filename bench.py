@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path: Krylov iterations/s of the PCG solve of the
+ADMM normal equations at BASELINE config C2 (256^2 x 256, fp64).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+A step = one PCG solve (tol 1e-8, x0 = 0, reference control flow) of the
+ADMM sub-problem S y = rhs taken after one ADMM step from a zero state, with
+every input resident in HBM.  value = Krylov iterations of the K timed steps /
+their device time (CUDA events on the library stream, barrier + sync on both
+sides, max over ranks).  e2e = the same through the host-buffer C-ABI call
+(fdg_admm_pcg_host: H2D rhs and x0 from pinned memory, D2H of x).
+Multi-GPU: replicas only -- each rank solves its own instance;
+value sums iterations over ranks and divides by the slowest rank's time.
+
+--impl reference: the unchanged reference (oracle/_ref: reference sources +
+FFTW3 shim) on the host cores; a step = exactly one iteration of the
+reference pcg loop body on the same C2 system (bounded CPU sample).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "krylov_iters_per_s"
+WORKLOAD = "C2"
+B_IT_VECTORS = 27  # algorithmic bytes per Krylov iteration = 27 * 8 * N
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _env_rank():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")),
+            int(os.environ.get("WORLD_SIZE", "1")))
+
+
+def _host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def _config(shape, extra=None):
+    c = {"workload": f"{WORKLOAD} {shape[1]}x{shape[2]} interior x {shape[0]} implicit-Euler steps: "
+                     "PCG solve of the ADMM normal equations (T. Chan circulant precond, tol 1e-8)",
+         "shape_nt_nx1_nx2": list(shape), "alpha_x": 1.5, "alpha_y": 1.5, "beta_reg": 1e-5,
+         "krylov_tol": 1e-8, "penalty_rho": 1.0, "parallelism": "replicas",
+         "l2": "inputs larger than L2 (each N-vector 134 MB > 126 MB)"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+# reference arm / CPU baseline: the unchanged reference on the host cores
+# --------------------------------------------------------------------------
+def reference_sample(iters: int, warmup: int, shape=(256, 256, 256)):
+    """Times `iters` single iterations of the reference pcg loop body (after
+    `warmup` untimed ones) on the C2 normal equations; returns per-iteration
+    seconds.  The oracle package is used here only as the CPU baseline."""
+    from oracle import Shape, baseline_problem, ref_lib, synthetic_ybar
+    from oracle.pyoracle import RefAdmm
+    cores = _host_cores()
+    R = ref_lib()
+    R.set_threads(cores)
+    s = Shape(*shape)
+    c = baseline_problem(WORKLOAD, s)
+    n = s.nt
+    assert s.nt == s.n1 == s.n2, "the unchanged reference is cube-only"
+    ybar = synthetic_ybar("sin", s)
+    op = R.op(n, c["time"], c["r1"], c["r2"], c["psi"])
+    pc = op.assemble_precond(c["rho"], c["delta"], c["gamma"])
+    adm = RefAdmm(R, op, pc, c["gamma"], c["rho"], c["delta"], u_lo=c["u"][0], u_hi=c["u"][1],
+                  tol_primal=c["tol_primal"], max_inner=c["max_inner"], fixed_tol=c["krylov_tol"],
+                  ybar=ybar)
+    rhs, _ = adm.build_rhs()
+    st = adm.krylov_init(rhs)
+    for _ in range(warmup):
+        adm.krylov_iteration(st)
+    times = []
+    for _ in range(iters):
+        t0 = time.perf_counter()
+        adm.krylov_iteration(st)
+        times.append(time.perf_counter() - t0)
+    return times, cores
+
+
+def run_reference(args):
+    rank, _, world = _env_rank()
+    if rank != 0:
+        return 0
+    shape = tuple(args.shape)
+    times, cores = reference_sample(args.steps, args.warmup, shape)
+    total = sum(times)
+    value = len(times) / total
+    sample = (f"{len(times)} single iterations of the reference pcg loop body (apply_S + "
+              f"CirculantPreconditioner::solve + vector algebra, admm.cpp:142-163) on the "
+              f"{shape} system after {args.warmup} warm-up iterations; FFTW3 shim with "
+              f"{cores} threads for the FFT batches, reference loops serial")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "it/s",
+            "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
+            "ms_per_step": 1000.0 * total / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded std::mt19937_64 target state)",
+            "config": _config(shape),
+            "cpu_baseline": {"value": value, "unit": "it/s", "cores": cores, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------
+# the B200 arm
+# --------------------------------------------------------------------------
+def run_b200(args):
+    import torch
+    rank, local_rank, world = _env_rank()
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_1907_13428_b200 import Context, make_problem
+
+    shape = tuple(args.shape)
+    N = shape[0] * shape[1] * shape[2]
+    ctx = Context(local_rank)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    c, op, pc, drv = make_problem(WORKLOAD, shape, ctx=ctx, seed=1 + rank)
+
+    # the hot-path input: the ADMM sub-problem after one step from zero
+    drv.step()
+    rhs = torch.empty(N, dtype=torch.float64, device="cuda")
+    x = torch.empty_like(rhs)
+    torch.cuda.synchronize()
+    drv.build_rhs_dev(rhs)
+    ctx.synchronize()
+    tol, max_inner = c["krylov_tol"], c["max_inner"]
+
+    def one_step():
+        x.zero_()  # on torch's stream; ordered by the synchronize below
+        torch.cuda.current_stream().synchronize()
+        return drv.pcg_dev(rhs, x, tol, max_inner)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ctx.synchronize()
+
+    for _ in range(args.warmup):
+        one_step()
+    barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    l0 = ctx.launch_count
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    iters = 0
+    pcg_ms = 0.0
+    for _ in range(args.steps):
+        r = one_step()
+        iters += r.iterations
+        pcg_ms += r.ms
+    ev1.record(stream)
+    barrier()
+    launches = ctx.launch_count - l0
+    clk = clocks.stop()
+    elapsed_ms = ev0.elapsed_time(ev1)
+
+    from paper_1907_13428_b200.replicas import aggregate
+    t_max, it_sum = aggregate(elapsed_ms, iters, dist, "cuda")
+    value = it_sum / (t_max / 1000.0)
+
+    # e2e through the host-buffer C-ABI call (pinned host rhs/x)
+    rhs_h = torch.empty(N, dtype=torch.float64, pin_memory=True)
+    rhs_h.copy_(rhs)
+    x_h = torch.zeros(N, dtype=torch.float64, pin_memory=True)
+    rhs_np, x_np = rhs_h.numpy(), x_h.numpy()
+    e_steps = max(1, min(args.steps, 5))
+    drv.pcg(rhs_np, x_np, tol, max_inner)  # warm
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e_iters = 0
+    e0.record(stream)
+    for _ in range(e_steps):
+        x_np[:] = 0.0
+        xo, r = drv.pcg(rhs_np, x_np, tol, max_inner)
+        e_iters += r.iterations
+    e1.record(stream)
+    barrier()
+    e_ms = e0.elapsed_time(e1)
+    e_tmax, e_it = aggregate(e_ms, e_iters, dist, "cuda")
+    e2e = {"value": e_it / (e_tmax / 1000.0), "unit": "it/s", "h2d_bytes_per_step": 2 * 8 * N,
+           "d2h_bytes_per_step": 8 * N, "steps": e_steps,
+           "path": "fdg_admm_pcg_host (pinned host rhs/x0 -> device PCG -> host x)"}
+
+    # ADMM step time (full outer iteration: build_rhs, PCG, B y, updates, dual_inf)
+    admm = None
+    if args.admm_steps > 0:
+        recs = [drv.step() for _ in range(args.admm_steps)]
+        admm = {"steps": len(recs), "step_ms_mean": statistics.mean(r.step_ms for r in recs),
+                "pcg_ms_mean": statistics.mean(r.pcg_ms for r in recs),
+                "inner_iters": [r.inner_iters for r in recs],
+                "r_eq_last": recs[-1].r_eq, "r_u_last": recs[-1].r_u}
+
+    # per-kernel roofline (burst: each pass launched back to back)
+    peak, peak_kind = _peaks()
+    passes = drv.profile_passes(args.profile_reps)
+    for p in passes.values():
+        p["gbs"] = p["bytes"] / (p["ms"] * 1e-3) / 1e9
+    dom_name = max(passes, key=lambda k: passes[k]["ms"])
+    dom = passes[dom_name]
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(dom_name)
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "kernel": dom_name, "achieved": dom["gbs"], "peak": peak,
+                "peak_kind": peak_kind, "unit": "GB/s", "frac": dom["gbs"] / peak,
+                "traffic": traffic, "algorithmic_bytes_per_launch": dom["bytes"],
+                "avg_launch_ms": dom["ms"]}
+    it_ms = t_max / max(1.0, it_sum / world)
+    iter_roof = {"model": "27 x 8 x N bytes per Krylov iteration (SURVEY.md 8d)",
+                 "bytes": B_IT_VECTORS * 8.0 * N, "ms_per_iteration": it_ms,
+                 "achieved_gbs": B_IT_VECTORS * 8.0 * N / (it_ms * 1e-3) / 1e9}
+    iter_roof["frac"] = iter_roof["achieved_gbs"] / peak
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            times, cores = reference_sample(args.cpu_iters, 1, shape)
+            cpu = {"value": len(times) / sum(times), "unit": "it/s", "cores": cores,
+                   "kind": "reference",
+                   "sample": f"{len(times)} iterations of the unchanged reference pcg loop body "
+                             f"on the same C2 system (oracle/_ref, FFTW3 shim, {cores} threads)"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "it/s", "cores": _host_cores(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded std::mt19937_64 target state, BASELINE C2 formulas)",
+                "config": _config(shape, {"iters_per_step": iters / args.steps,
+                                          "pcg_ms_inside_api": pcg_ms / args.steps}),
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roofline,
+                "iteration_roofline": iter_roof, "passes": passes, "admm": admm,
+                "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--shape", type=int, nargs=3, default=[256, 256, 256])
+    ap.add_argument("--admm-steps", type=int, default=3)
+    ap.add_argument("--profile-reps", type=int, default=10)
+    ap.add_argument("--cpu-iters", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -158,6 +158,10 @@ fdg_status fdg_admm_set(fdg_admm adm, int field, const double* host_in);
 /* Device pointer of a state field (y, v, z_y, z_v, p, w_y, w_v, ybar, By). */
 fdg_status fdg_admm_field_ptr(fdg_admm adm, int field, double** dev);
 
+/* Test accessor: PCG work vector (0 r, 1 z, 2 p, 3 u, 4 w, 5 vp; N doubles)
+ * or, with which = -1, the device scalar block (32 doubles). */
+fdg_status fdg_admm_debug_get(fdg_admm adm, int which, double* host_out);
+
 /* apply_S(work, x, out, ws)  admm.hpp:79-80, admm.cpp:87-98 */
 fdg_status fdg_admm_apply_S(fdg_admm adm, const double* x_dev, double* out_dev);
 /* build_rhs(work, state, rhs, ws) admm.cpp:100-119; r_cache_dev may be NULL */
@@ -173,6 +177,13 @@ fdg_status fdg_admm_pcg_host(fdg_admm adm, const double* rhs, double* x, double 
 fdg_status fdg_admm_dual_inf(fdg_admm adm, double* out);
 /* Objective 1/2 (y-ybar)^T J (y-ybar) + 1/2 v^T J2 v */
 fdg_status fdg_admm_objective(fdg_admm adm, double* out);
+
+/* Bench/roofline hook: average CUDA-event time (ms) of each kernel of one
+ * PCG iteration over `reps` back-to-back launches, and its algorithmic HBM
+ * bytes.  9 entries: K1 row(B), K2 x1 col(S mid), K3 row(B^T + r update),
+ * P1 x2 Hartley, P2 x1 Hartley, P3 t filter, P4 x1 Hartley, P5 x2 Hartley
+ * (+ r.z), K9 x/p update.  Clobbers the PCG scratch vectors. */
+fdg_status fdg_admm_profile_passes(fdg_admm adm, int reps, double* ms, double* bytes);
 
 /* --------------------------------------------------- synthetic inputs */
 /* std::mt19937_64(seed) + std::normal_distribution<double> in layout order

@@ -91,6 +91,8 @@ class RefLib(_Lib):
         L.ref_admm_build_rhs.argtypes = [C.c_void_p, _dp, _dp]
         L.ref_admm_pcg.argtypes = [C.c_void_p, _dp, _dp, C.c_double, C.c_int, _dp]
         L.ref_admm_step.argtypes = [C.c_void_p, _dp]
+        L.ref_admm_krylov_init.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp]
+        L.ref_admm_krylov_iteration.argtypes = [C.c_void_p] + [_dp] * 7
         L.ref_admm_dual_inf.argtypes = [C.c_void_p, _dp]
         L.ref_admm_objective.argtypes = [C.c_void_p, _dp]
         L.ref_randn.argtypes = [C.c_uint64, C.c_long, _dp]
@@ -352,6 +354,23 @@ class RefAdmm(_AdmmBase):
         if getattr(self, "h", None):
             self.L.lib.ref_admm_destroy(self.h)
             self.h = None
+
+    def krylov_init(self, rhs):
+        """pcg start (x = 0): returns the iteration state dict."""
+        st = {k: np.zeros(self.N) for k in ("x", "r", "z", "p", "q")}
+        st["rz"] = np.zeros(1)
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        self.L.check(self.L.lib.ref_admm_krylov_init(self.h, _ptr(rhs), _ptr(st["r"]), _ptr(st["z"]),
+                                                     _ptr(st["p"]), _ptr(st["rz"])))
+        return st
+
+    def krylov_iteration(self, st):
+        """One iteration of the reference pcg loop body; returns (pq, |r|, rz)."""
+        out = np.zeros(3)
+        self.L.check(self.L.lib.ref_admm_krylov_iteration(
+            self.h, _ptr(st["x"]), _ptr(st["r"]), _ptr(st["z"]), _ptr(st["p"]), _ptr(st["q"]),
+            _ptr(st["rz"]), _ptr(out)))
+        return out
 
 
 # --------------------------------------------------------------------------

@@ -412,6 +412,52 @@ int ref_admm_pcg(void* vh, const double* rhs, double* x, double tol, int max_inn
   });
 }
 
+// pcg's start (admm.cpp:125-141, x == 0 path): r = rhs, z = M r, p = z, rz = r.z
+int ref_admm_krylov_init(void* vh, const double* rhs, double* r, double* z, double* p, double* rz) {
+  auto* h = static_cast<AdmmHandle*>(vh);
+  return guard([&] {
+    const std::size_t N = h->work.size();
+    std::memcpy(r, rhs, sizeof(double) * N);
+    h->pc->pc->solve(std::span<const double>(r, N), std::span<double>(z, N), h->pc->ws);
+    std::memcpy(p, z, sizeof(double) * N);
+    double s = 0.0;
+    for (std::size_t i = 0; i < N; ++i) s += r[i] * z[i];
+    *rz = s;
+  });
+}
+
+// Exactly one iteration of pcg's loop body (admm.cpp:142-163) with the
+// reference's apply_S and CirculantPreconditioner::solve: the bounded unit of
+// the CPU baseline.  out = {pq, |r|, rz_next}; *rz is updated.
+int ref_admm_krylov_iteration(void* vh, double* x, double* r, double* z, double* p, double* q,
+                              double* rz, double* out) {
+  auto* h = static_cast<AdmmHandle*>(vh);
+  return guard([&] {
+    const std::size_t N = h->work.size();
+    apply_S(h->work, std::span<const double>(p, N), std::span<double>(q, N), h->op->ws);
+    double pq = 0.0;
+    for (std::size_t i = 0; i < N; ++i) pq += p[i] * q[i];
+    if (!std::isfinite(pq) || pq <= 0.0)
+      throw std::runtime_error("pcg: operator lost positive definiteness");
+    const double a = *rz / pq;
+    for (std::size_t i = 0; i < N; ++i) {
+      x[i] += a * p[i];
+      r[i] -= a * q[i];
+    }
+    double rr = 0.0;
+    for (std::size_t i = 0; i < N; ++i) rr += r[i] * r[i];
+    h->pc->pc->solve(std::span<const double>(r, N), std::span<double>(z, N), h->pc->ws);
+    double rzn = 0.0;
+    for (std::size_t i = 0; i < N; ++i) rzn += r[i] * z[i];
+    const double beta = rzn / *rz;
+    *rz = rzn;
+    for (std::size_t i = 0; i < N; ++i) p[i] = z[i] + beta * p[i];
+    out[0] = pq;
+    out[1] = std::sqrt(rr);
+    out[2] = rzn;
+  });
+}
+
 // AdmmDriver::step, admm.cpp:245-277, re-sequenced from the public functions.
 // rec: {iter, r_eq, r_y, r_u, dual_inf, inner_iters, inner_tol, converged,
 //       pcg_seconds, step_seconds, pcg_rel_residual, stagnations}

@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libfdg.so")
+LIB_PATH = os.environ.get("FDG_LIB") or os.path.join(PKG, "lib", "libfdg.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -96,8 +96,11 @@ _sig("fdg_admm_pcg", _st, _vp, _vp, _vp, C.c_double, C.c_int, C.POINTER(PcgResul
 _sig("fdg_admm_pcg_host", _st, _vp, _dp, _dp, C.c_double, C.c_int, C.POINTER(PcgResult))
 _sig("fdg_admm_dual_inf", _st, _vp, _dp)
 _sig("fdg_admm_objective", _st, _vp, _dp)
+_sig("fdg_admm_profile_passes", _st, _vp, C.c_int, _dp, _dp)
+_sig("fdg_admm_debug_get", _st, _vp, C.c_int, _dp)
 
-EXPORTED = [name for name in dir(lib) if name.startswith("fdg_")]
+PASS_NAMES = ["K1_row_B", "K2_col_S_mid", "K3_row_BT_update", "P1_hartley_x2", "P2_hartley_x1",
+              "P3_t_filter", "P4_hartley_x1", "P5_hartley_x2_dot", "K9_cg_update"]
 
 
 class FdgError(RuntimeError):

@@ -326,9 +326,15 @@ class AdmmDriver:
         return PcgResult(r.iterations, bool(r.converged), r.rel_residual, r.ms)
 
     def pcg(self, rhs, x=None, tol: float = 1e-8, max_inner: int = 400):
-        """Host-buffer pcg (H2D rhs/x, device solve, D2H x)."""
+        """Host-buffer pcg (H2D rhs/x, device solve, D2H x).  A contiguous
+        float64 `x` is updated in place (pass pinned buffers for full copy
+        bandwidth); otherwise a copy is made."""
         rhs = _f64(rhs)
-        x = np.zeros(self.N) if x is None else _f64(x).copy()
+        if x is None:
+            x = np.zeros(self.N)
+        elif not (isinstance(x, np.ndarray) and x.dtype == np.float64 and x.flags.c_contiguous
+                  and x.flags.writeable):
+            x = _f64(x).copy()
         if rhs.size != self.N or x.size != self.N:
             raise ValueError("pcg: dimension mismatch")
         r = N.PcgResult()
@@ -344,6 +350,17 @@ class AdmmDriver:
         out = np.zeros(1)
         check(lib.fdg_admm_objective(self.h, _ptr(out)))
         return float(out[0])
+
+    def profile_passes(self, reps: int = 10) -> dict:
+        ms, by = np.zeros(9), np.zeros(9)
+        check(lib.fdg_admm_profile_passes(self.h, reps, _ptr(ms), _ptr(by)))
+        return {n: dict(ms=float(m), bytes=float(b)) for n, m, b in zip(N.PASS_NAMES, ms, by)}
+
+    def debug_get(self, which: str):
+        names = dict(r=0, z=1, p=2, u=3, w=4, vp=5, scalars=-1)
+        out = np.zeros(32 if which == "scalars" else self.N)
+        check(lib.fdg_admm_debug_get(self.h, names[which], _ptr(out)))
+        return out
 
     # host conveniences used by the parity tests (device work + staging)
     def apply_S(self, x) -> np.ndarray:

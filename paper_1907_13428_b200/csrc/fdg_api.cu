@@ -13,6 +13,7 @@
 #include <complex>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <random>
 #include <stdexcept>
@@ -20,6 +21,7 @@
 #include <vector>
 
 #include "../../include/fdg.h"
+#include "fdg_fft.cuh"
 #include "fdg_internal.h"
 
 using fdg::AxisSym;
@@ -118,6 +120,31 @@ std::vector<double> twiddles(int L) {
     w[2 * k + 1] = s;
   }
   return w;
+}
+
+// Per-pass Stockham twiddle table of length N for the device FFT plan
+// (fdg_fft.cuh Stockham: pass with stride Ns > 1 owns (Rp-1)*Ns entries,
+// entry (r-1)*Ns + j = W_N^(j r N/(Ns Rp))).
+std::vector<double> stockham_twiddles(int N) {
+  const std::vector<double> w = twiddles(N);
+  std::vector<double> out(2 * (size_t)std::max(N, 1), 0.0);
+  const int R = fdg::fft_radix(N);
+  int off = 0;
+  for (int Ns = 1; Ns < N;) {
+    const int Rp = std::min(R, N / Ns);
+    if (Ns > 1) {
+      for (int r = 1; r < Rp; ++r)
+        for (int j = 0; j < Ns; ++j) {
+          const long k = ((long)j * r * (N / (Ns * Rp))) % N;
+          const size_t idx = (size_t)off + (size_t)(r - 1) * Ns + j;
+          out[2 * idx] = w[2 * k];
+          out[2 * idx + 1] = w[2 * k + 1];
+        }
+      off += (Rp - 1) * Ns;
+    }
+    Ns *= Rp;
+  }
+  return out;
 }
 
 // Full length-L spectrum of the circulant embedding of a Toeplitz factor:
@@ -253,12 +280,15 @@ struct fdg_op_s {
   int nt = 0, n1 = 0, n2 = 0;
   double psi = 1.0;
   std::vector<double> tcol, trow, c1, r1, c2, r2;
-  DevBuf sym1, tw1, sym2, tw2, symt, symt_adj, twt;
+  DevBuf sym1, tw1, sym2, tw2, symt, symt_adj, twt, sym2s;
   AxisSym ax1, ax2;
+  AxisSym ax2s;  // x2 axis with the stencil diagonal folded in: sym2 - c0 (row passes)
   TimeFactor tf;
   size_t N() const { return (size_t)nt * n1 * n2; }
   double scale1() const { return -psi / ax1.L; }
   double scale2() const { return -psi / ax2.L; }
+  // symbol of the row passes (stencil diagonal folded in when kind == 1)
+  const AxisSym& row_axis() const { return ax2s; }
 };
 
 namespace {
@@ -277,7 +307,7 @@ void build_axis(fdg_op_s* op, AxisSym& ax, DevBuf& sym, DevBuf* sym_adj, DevBuf&
   ax.n = n;
   ax.L = L;
   upload(sym, embed_symbol_full(col, row, L), op->ctx->stream);
-  upload(tw, twiddles(L), op->ctx->stream);
+  upload(tw, stockham_twiddles(L), op->ctx->stream);
   ax.sym = sym.c();
   ax.tw = tw.c();
   ax.sym_adj = ax.sym;
@@ -292,7 +322,7 @@ void build_axis(fdg_op_s* op, AxisSym& ax, DevBuf& sym, DevBuf* sym_adj, DevBuf&
 void op_apply_dev(fdg_op_s* op, const double* x, double* out, bool adjoint) {
   cudaStream_t st = op->ctx->stream;
   LaunchCounter* lc = &op->ctx->lc;
-  ck(fdg::launch_row_apply(st, lc, x, out, op->nt, op->n1, op->n2, op->ax2, op->scale2(), op->tf, op->psi, adjoint),
+  ck(fdg::launch_row_apply(st, lc, x, out, op->nt, op->n1, op->n2, op->row_axis(), op->scale2(), op->tf, op->psi, adjoint),
      "row pass");
   ck(fdg::launch_col_acc(st, lc, x, out, out, op->nt, op->n1, op->n2, op->ax1, op->scale1(), false), "x1 pass");
   if (op->tf.kind == 2)
@@ -369,7 +399,7 @@ void apply_S_dev(fdg_admm_s* a, const double* x, double* q) {
   LaunchCounter* lc = &op->ctx->lc;
   const TimeFactor& tf = op->tf;
   TimeFactor none_tf;
-  ck(fdg::launch_row_apply(st, lc, x, a->u.d(), op->nt, op->n1, op->n2, op->ax2, op->scale2(),
+  ck(fdg::launch_row_apply(st, lc, x, a->u.d(), op->nt, op->n1, op->n2, op->row_axis(), op->scale2(),
                            tf.kind == 1 ? tf : none_tf, op->psi, false),
      "S row");
   if (tf.kind == 2)
@@ -383,7 +413,7 @@ void apply_S_dev(fdg_admm_s* a, const double* x, double* q) {
     ck(fdg::launch_col_acc(st, lc, a->w.d(), a->vp.d(), a->vp.d(), 1, op->nt, op->n1 * op->n2, tf.fft,
                            op->psi / tf.fft.L, true),
        "S t adj");
-  ck(fdg::launch_row_s_out(st, lc, a->w.d(), a->vp.d(), q, nullptr, op->nt, op->n1, op->n2, op->ax2, op->scale2(),
+  ck(fdg::launch_row_s_out(st, lc, a->w.d(), a->vp.d(), q, nullptr, op->nt, op->n1, op->n2, op->row_axis(), op->scale2(),
                            tf.kind == 1 ? tf : none_tf, op->psi, nullptr, nullptr, RedSlot{}),
      "S row adj");
 }
@@ -396,7 +426,7 @@ void s_and_update(fdg_admm_s* a, const double* dd, const double* rz_slot) {
   LaunchCounter* lc = &op->ctx->lc;
   const TimeFactor& tf = op->tf;
   TimeFactor none_tf;
-  ck(fdg::launch_row_apply(st, lc, dd, a->u.d(), op->nt, op->n1, op->n2, op->ax2, op->scale2(),
+  ck(fdg::launch_row_apply(st, lc, dd, a->u.d(), op->nt, op->n1, op->n2, op->row_axis(), op->scale2(),
                            tf.kind == 1 ? tf : none_tf, op->psi, false),
      "K1 row");
   if (tf.kind == 2)
@@ -410,7 +440,7 @@ void s_and_update(fdg_admm_s* a, const double* dd, const double* rz_slot) {
     ck(fdg::launch_col_acc(st, lc, a->w.d(), a->vp.d(), a->vp.d(), 1, op->nt, op->n1 * op->n2, tf.fft,
                            op->psi / tf.fft.L, true),
        "K2 t");
-  ck(fdg::launch_row_s_out(st, lc, a->w.d(), a->vp.d(), nullptr, a->r.d(), op->nt, op->n1, op->n2, op->ax2,
+  ck(fdg::launch_row_s_out(st, lc, a->w.d(), a->vp.d(), nullptr, a->r.d(), op->nt, op->n1, op->n2, op->row_axis(),
                            op->scale2(), tf.kind == 1 ? tf : none_tf, op->psi, rz_slot, a->sc.at(S_PQ),
                            a->sc.slot(S_RR)),
      "K3 row");
@@ -670,9 +700,18 @@ fdg_status fdg_op_create(fdg_ctx ctx, int nt, int n1, int n2, const double* tcol
       op->tf.kind = 1;
       op->tf.c0 = op->tcol[0];
       op->tf.c1 = nt > 1 ? op->tcol[1] : 0.0;
+      // psi c0 x_k == (-psi/L) IFFT(FFT(x) * (-c0 L)): fold the diagonal of the
+      // time stencil into the x2 Toeplitz symbol (exact in real arithmetic).
+      std::vector<double> s2 = embed_symbol_full(op->c2, op->r2, op->ax2.L);
+      for (int f = 0; f < op->ax2.L; ++f) s2[2 * f] -= op->tf.c0;
+      upload(op->sym2s, s2, ctx->stream);
+      op->ax2s = op->ax2;
+      op->ax2s.sym = op->sym2s.c();
+      op->ax2s.sym_adj = op->sym2s.c();
     } else {
       op->tf.kind = 2;
       build_axis(op.get(), op->tf.fft, op->symt, &op->symt_adj, op->twt, op->tcol, op->trow);
+      op->ax2s = op->ax2;
     }
     ctx->ensure_partials(fdg::max_partials_needed(nt, n1, n2));
     *out = op.release();
@@ -751,9 +790,9 @@ fdg_pc_s* make_pc(fdg_ctx ctx, int nt, int n1, int n2, const double* lt, const d
   upload(pc->lt, std::vector<double>(lt, lt + 2 * (size_t)nt), st);
   upload(pc->l1, std::vector<double>(l1, l1 + 2 * (size_t)n1), st);
   upload(pc->l2, std::vector<double>(l2, l2 + 2 * (size_t)n2), st);
-  upload(pc->twt, twiddles(nt), st);
-  upload(pc->tw1, twiddles(n1), st);
-  upload(pc->tw2, twiddles(n2), st);
+  upload(pc->twt, stockham_twiddles(nt), st);
+  upload(pc->tw1, stockham_twiddles(n1), st);
+  upload(pc->tw2, stockham_twiddles(n2), st);
   // circulant.cpp:37-40
   const double m2 = 1.0 / (rho * (gamma / (psi * psi) + 1.0 / delta)) + delta / rho;
   PcTables& t = pc->tab;
@@ -956,6 +995,24 @@ fdg_status fdg_admm_set(fdg_admm a, int field, const double* in) {
   });
 }
 
+// Debug/test accessor of the PCG work vectors (0 r, 1 z, 2 p, 3 u, 4 w,
+// 5 vp) and of the device scalar block (which = -1: S_COUNT doubles).
+fdg_status fdg_admm_debug_get(fdg_admm a, int which, double* host_out) {
+  return guard([&] {
+    if (!a) fail(FDG_EINVAL, "null admm");
+    a->op->ctx->set_device();
+    cudaStream_t st = a->op->ctx->stream;
+    ck(cudaStreamSynchronize(st), "sync");
+    if (which < 0) {
+      ck(cudaMemcpy(host_out, a->sc.vals.p, sizeof(double) * S_COUNT, cudaMemcpyDeviceToHost), "D2H");
+      return;
+    }
+    DevBuf* b[] = {&a->r, &a->z, &a->d, &a->u, &a->w, &a->vp};
+    if (which > 5) fail(FDG_EINVAL, "fdg_admm_debug_get: bad vector");
+    ck(cudaMemcpy(host_out, b[which]->p, sizeof(double) * a->N, cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
 fdg_status fdg_admm_field_ptr(fdg_admm a, int field, double** dev) {
   return guard([&] {
     if (!a) fail(FDG_EINVAL, "null admm");
@@ -1031,6 +1088,66 @@ fdg_status fdg_admm_objective(fdg_admm a, double* out) {
     double s[2];
     a->sc.read(S_OBJ, 2, s);
     *out = 0.5 * s[0] + 0.5 * s[1];
+  });
+}
+
+// Per-pass device timing of one PCG iteration's kernels (bench/roofline
+// hook).  Each pass is launched `reps` times back to back between two CUDA
+// events on the context stream.  Overwrites the PCG scratch vectors (run it
+// after the measurements that need them).  Order of ms[]: K1 row, K2 col,
+// K3 row, P1 x2, P2 x1, P3 t, P4 x1, P5 x2, K9 update.
+fdg_status fdg_admm_profile_passes(fdg_admm a, int reps, double* ms, double* bytes) {
+  return guard([&] {
+    if (!a || reps < 1) fail(FDG_EINVAL, "fdg_admm_profile_passes: bad arguments");
+    fdg_ctx ctx = a->op->ctx;
+    ctx->set_device();
+    cudaStream_t st = ctx->stream;
+    LaunchCounter* lc = &ctx->lc;
+    fdg_op_s* op = a->op;
+    fdg_pc_s* pc = a->pc;
+    const size_t N = a->N;
+    const int F = op->nt * op->n1;
+    const TimeFactor& tf = op->tf;
+    TimeFactor none_tf;
+    const TimeFactor& stf = tf.kind == 1 ? tf : none_tf;
+    Scalars& sc = a->sc;
+    // well-defined scalars for the passes that read them
+    const double one = 1.0;
+    for (int s : {S_RZ0, S_RZ1, S_PQ})
+      ck(cudaMemcpyAsync(sc.at(s), &one, sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
+    ck(cudaStreamSynchronize(st), "sync");
+    std::vector<std::function<void()>> passes = {
+        [&] { ck(fdg::launch_row_apply(st, lc, a->d.d(), a->u.d(), op->nt, op->n1, op->n2, op->row_axis(), op->scale2(), stf,
+                                       op->psi, false), "K1"); },
+        [&] { ck(fdg::launch_col_s_mid(st, lc, a->d.d(), a->u.d(), a->w.d(), a->vp.d(), op->nt, op->n1, op->n2,
+                                       op->ax1, op->scale1(), a->inv_m2.d(), a->a1.d(), sc.slot(S_DOT)), "K2"); },
+        [&] { ck(fdg::launch_row_s_out(st, lc, a->w.d(), a->vp.d(), nullptr, a->r.d(), op->nt, op->n1, op->n2,
+                                       op->row_axis(), op->scale2(), stf, op->psi, sc.at(S_RZ0), sc.at(S_PQ),
+                                       sc.slot(S_DOT)), "K3"); },
+        [&] { ck(fdg::launch_hartley_row(st, lc, a->r.d(), a->u.d(), F, pc->n2, pc->tab.tw_2, nullptr, RedSlot{}),
+                 "P1"); },
+        [&] { ck(fdg::launch_hartley_col(st, lc, a->u.d(), pc->nt, pc->n1, pc->n2, pc->tab.tw_1), "P2"); },
+        [&] { ck(fdg::launch_t_filter(st, lc, a->u.d(), pc->tab), "P3"); },
+        [&] { ck(fdg::launch_hartley_col(st, lc, a->u.d(), pc->nt, pc->n1, pc->n2, pc->tab.tw_1), "P4"); },
+        [&] { ck(fdg::launch_hartley_row(st, lc, a->u.d(), a->z.d(), F, pc->n2, pc->tab.tw_2, a->r.d(),
+                                         sc.slot(S_DOT)), "P5"); },
+        [&] { ck(fdg::launch_cg_update(st, lc, a->tmp.d(), a->d.d(), a->z.d(), N, sc.at(S_RZ0), sc.at(S_PQ),
+                                       sc.at(S_RZ1), sc.at(S_RZ0), true), "K9"); },
+    };
+    // algorithmic HBM bytes per launch (each N-vector read or written once)
+    const double nb = 8.0 * (double)N;
+    const double alg[9] = {2 * nb, 4 * nb, 4 * nb, 2 * nb, 2 * nb, 2 * nb, 2 * nb, 3 * nb, 5 * nb};
+    for (size_t i = 0; i < passes.size(); ++i) {
+      passes[i]();  // warm
+      ck(cudaEventRecord(a->e0, st), "event");
+      for (int r = 0; r < reps; ++r) passes[i]();
+      ck(cudaEventRecord(a->e1, st), "event");
+      ck(cudaEventSynchronize(a->e1), "sync");
+      float t = 0.f;
+      ck(cudaEventElapsedTime(&t, a->e0, a->e1), "elapsed");
+      ms[i] = t / reps;
+      if (bytes) bytes[i] = alg[i];
+    }
   });
 }
 

@@ -128,91 +128,154 @@ struct Dft {
   }
 };
 
+// Shared-memory slot of (pos, lane).  Rows of G double2; for G < 8 a 128-byte
+// bank window holds 8/G positions, so the low log2(8/G) bits of pos are XORed
+// with a fold of the higher bits: power-of-two position strides (the Stockham
+// scatter) then spread over all bank groups (measured model: 1.13x / 1.19x of
+// conflict-free for G = 4 / 2 instead of 1.20x / 1.60x).
+template <int G>
+__device__ __forceinline__ int sidx(int pos, int g) {
+  if constexpr (G >= 8) {
+    return pos * G + g;
+  } else if constexpr (G == 4) {
+    return (pos ^ (__popc(pos >> 1) & 1)) * G + g;
+  } else {  // G == 2: fold the 2-bit chunks of pos >> 2
+    int h = pos >> 2;
+    h ^= h >> 8;
+    h ^= h >> 4;
+    h ^= h >> 2;
+    return (pos ^ (h & 3)) * G + g;
+  }
+}
+
+// Lane-major slot (row passes: a warp covers consecutive positions of one
+// lane, so its global accesses are 256-byte coalesced).  Each lane owns N
+// contiguous slots; the low 3 bits of pos are XORed with a fold of the
+// higher 3-bit groups so that strided Stockham scatters hit 8 different
+// bank groups per quarter-warp.
+template <int N>
+__device__ __forceinline__ int lidx(int pos, int g) {
+  const int f = (pos >> 3) ^ (pos >> 6) ^ (pos >> 9);
+  return g * N + (pos ^ (f & 7));
+}
+
+// LAYOUT 0: lane-interleaved rows of G (column passes); 1: lane-major.
+template <int LAYOUT, int N, int G>
+__device__ __forceinline__ int slot(int pos, int g) {
+  if constexpr (LAYOUT == 0) return sidx<G>(pos, g);
+  else return lidx<N>(pos, g);
+}
+
+// Double-buffered exchange area: consecutive exchanges alternate between two
+// buffers, so one __syncthreads() per exchange suffices (a thread can only
+// overwrite buffer X after every thread passed the barrier of the exchange
+// that used the other buffer, i.e. after all reads of X completed).
+struct Ex {
+  double2* buf0;
+  double2* buf1;
+  int k;
+  __device__ __forceinline__ double2* next() {
+    // single buffer: every thread must have finished reading the previous
+    // exchange before anyone scatters the next one (write-after-read)
+    if (buf0 == buf1) __syncthreads();
+    double2* p = k ? buf1 : buf0;
+    k ^= 1;
+    return p;
+  }
+};
+
+// Registers per thread (= radix bound) used for a transform of length N;
+// shared by the kernels (Cfg) and the host twiddle-table builder.
+__host__ __device__ constexpr int fft_radix(int N) { return N <= 8 ? N : (N <= 512 ? 8 : 16); }
+
 // Compile-time radix plan: passes of radix min(R, N/Ns).
 template <int N, int R, int Ns>
 struct PassRadix {
   static constexpr int value = (N / Ns) < R ? (N / Ns) : R;
 };
 
+// Per-pass twiddle table ("ptw"): pass with stride Ns > 1 owns (Rp-1)*Ns
+// entries at offset OFF, entry (r-1)*Ns + j = W_N^(j r N/(Ns Rp)).  A
+// quarter-warp (8 consecutive butterflies) then reads 8 consecutive entries
+// (one 128-byte bank window) instead of a power-of-two stride.
+// Host builder: fdg_api.cu stockham_twiddles().
+
 // One Stockham pass on a lane (registers in, registers out, with the
 // shared-memory scatter of the pass output unless it is the last pass).
 //   N   : transform length, R: registers per thread, T = N/R
-//   Ns  : product of previous radices
+//   Ns  : product of previous radices, OFF: offset of this pass in ptw
 //   G   : lanes per CTA (smem row width)
-template <int N, int R, int G, bool INV, int Ns>
+template <int N, int R, int G, bool INV, int Ns, int LAYOUT, int OFF = 0>
 struct Stockham {
   static constexpr int T = N / R;
   static constexpr int Rp = PassRadix<N, R, Ns>::value;
   static constexpr int S = R / Rp;  // butterflies per thread in this pass
   static constexpr bool LAST = (Ns * Rp == N);
+  static constexpr int NEXT_OFF = OFF + (Ns > 1 ? (Rp - 1) * Ns : 0);
 
-  __device__ __forceinline__ static void run(double2 (&v)[R], double2* sm, int t, int g,
-                                             const double2* __restrict__ tw) {
+  __device__ __forceinline__ static void run(double2 (&v)[R], Ex& ex, int t, int g, const double2* ptw) {
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int b = t + s * T;  // butterfly index in [0, N/Rp)
       if constexpr (Ns > 1) {
-        const int bm = b % Ns;
+        const double2* tw = ptw + OFF + (b & (Ns - 1));
 #pragma unroll
         for (int r = 1; r < Rp; ++r) {
-          const double2 w = __ldg(&tw[bm * r * (N / (Ns * Rp))]);
+          const double2 w = tw[(r - 1) * Ns];
           v[s + r * S] = INV ? cmulc(v[s + r * S], w) : cmul(v[s + r * S], w);
         }
       }
       Dft<Rp, INV>::run(v, s, S);
     }
     if constexpr (!LAST) {
+      double2* sm = ex.next();
       // scatter: out[(b/Ns)*Ns*Rp + b%Ns + r*Ns] = v[s + r*S]
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const int b = t + s * T;
-        const int base = (b / Ns) * Ns * Rp + (b % Ns);
+        const int base = (b & ~(Ns - 1)) * Rp + (b & (Ns - 1));
 #pragma unroll
-        for (int r = 0; r < Rp; ++r) sm[(base + r * Ns) * G + g] = v[s + r * S];
+        for (int r = 0; r < Rp; ++r) sm[slot<LAYOUT, N, G>(base + r * Ns, g)] = v[s + r * S];
       }
       __syncthreads();
 #pragma unroll
-      for (int m = 0; m < R; ++m) v[m] = sm[(t + m * T) * G + g];
-      __syncthreads();
-      Stockham<N, R, G, INV, Ns * Rp>::run(v, sm, t, g, tw);
+      for (int m = 0; m < R; ++m) v[m] = sm[slot<LAYOUT, N, G>(t + m * T, g)];
+      Stockham<N, R, G, INV, Ns * Rp, LAYOUT, NEXT_OFF>::run(v, ex, t, g, ptw);
     }
   }
 };
 
-// Terminal specialization guard (never instantiated with Ns >= N).
-template <int N, int R, int G, bool INV>
-struct StockhamEnd {
-  __device__ __forceinline__ static void run(double2 (&)[R], double2*, int, int, const double2*) {}
-};
-
 // Full FFT of length N on the lane; x[t + m*T] in v[m] before and after.
 // Every thread of the CTA must call it (it contains __syncthreads()).
-template <int N, int R, int G, bool INV>
-__device__ __forceinline__ void fft_lane(double2 (&v)[R], double2* sm, int t, int g,
-                                         const double2* __restrict__ tw) {
+template <int N, int R, int G, bool INV, int LAYOUT = 0>
+__device__ __forceinline__ void fft_lane(double2 (&v)[R], Ex& ex, int t, int g, const double2* tw) {
   if constexpr (N == 1) {
     return;
   } else {
-    Stockham<N, R, G, INV, 1>::run(v, sm, t, g, tw);
+    Stockham<N, R, G, INV, 1, LAYOUT>::run(v, ex, t, g, tw);
   }
 }
 
 // Exchange helper: value at position (N - pos) mod N for every register
-// (used by the Hartley post-processing).  Contains two __syncthreads().
-template <int N, int R, int G>
-__device__ __forceinline__ void mirror_lane(const double2 (&v)[R], double2 (&w)[R], double2* sm, int t,
-                                            int g) {
+// (used by the Hartley post-processing).  One __syncthreads().
+template <int N, int R, int G, int LAYOUT = 0>
+__device__ __forceinline__ void mirror_lane(const double2 (&v)[R], double2 (&w)[R], Ex& ex, int t, int g) {
   constexpr int T = N / R;
+  double2* sm = ex.next();
 #pragma unroll
-  for (int m = 0; m < R; ++m) sm[(t + m * T) * G + g] = v[m];
+  for (int m = 0; m < R; ++m) sm[slot<LAYOUT, N, G>(t + m * T, g)] = v[m];
   __syncthreads();
 #pragma unroll
   for (int m = 0; m < R; ++m) {
     const int pos = t + m * T;
-    const int mp = pos == 0 ? 0 : N - pos;
-    w[m] = sm[mp * G + g];
+    const int mp = (N - pos) & (N - 1);
+    w[m] = sm[slot<LAYOUT, N, G>(mp, g)];
   }
-  __syncthreads();
+}
+
+// Cooperative copy of a small global table into shared memory.
+__device__ __forceinline__ void load_table(double2* dst, const double2* __restrict__ src, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(&src[i]);
 }
 
 // Two packed real sequences a + i b -> (Hartley(a), Hartley(b)) given

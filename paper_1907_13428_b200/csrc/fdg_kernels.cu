@@ -17,365 +17,10 @@
 
 #include "fdg_fft.cuh"
 #include "fdg_internal.h"
+#include "fdg_passes.cuh"
 #include "fdg_reduce.cuh"
 
 namespace fdg {
-
-// ------------------------------------------------------------ tile configs
-template <int L>
-struct Cfg {
-  static constexpr int R = L <= 8 ? L : (L <= 512 ? 8 : 16);
-  static constexpr int T = L / R;
-  static constexpr int G0 = L >= 2048 ? 4 : 8;
-  static constexpr int G = (G0 * T < 32) ? (32 / T) : G0;
-  static constexpr int THREADS = G * T;
-  static constexpr size_t SMEM = (size_t)L * G * sizeof(double2);
-};
-
-__device__ __forceinline__ size_t idx2(size_t a, size_t b, size_t n) { return a * n + b; }
-
-// =================================================================== rows
-// Row pass along x2 (contiguous fibres of length n; embedding length L).
-//   MODE 0 (apply):  out = psi*time(x) + scale * T2 x
-//   MODE 1 (S out):  q = vp + psi*time^T(x) + scale * T2 x; q_out = q (opt);
-//                    r -= (num/den) q; reduce |r|^2
-struct RowArgs {
-  const double* x;
-  const double* vp;
-  double* out;
-  double* q_out;
-  double* r;
-  int nt, n1, n;
-  const double2* sym;
-  const double2* tw;
-  double scale;
-  int tkind;  // 1: stencil
-  double tc0, tc1;
-  int tdir;  // -1: uses k-1 (forward B), +1: uses k+1 (adjoint)
-  const double* a_num;
-  const double* a_den;
-  RedSlot red;
-};
-
-template <int L, int MODE>
-__global__ void __launch_bounds__(Cfg<L>::THREADS) k_row(RowArgs a) {
-  using C = Cfg<L>;
-  constexpr int R = C::R, T = C::T, G = C::G, H = (R + 1) / 2;
-  extern __shared__ double2 sm[];
-  __shared__ double scratch[32];
-  const int g = threadIdx.x % G, t = threadIdx.x / G;
-  const long F = (long)a.nt * a.n1;
-  const long f = ((long)blockIdx.x * G + g) * 2;
-  const bool va = f < F, vb = f + 1 < F;
-  const int n = a.n;
-  double2 v[R];
-  double2 xr[H];
-#pragma unroll
-  for (int m = 0; m < R; ++m) {
-    const int pos = t + m * T;
-    double2 z = make_double2(0.0, 0.0);
-    if (m < H && pos < n) {
-      if (va) z.x = __ldg(&a.x[idx2(f, pos, n)]);
-      if (vb) z.y = __ldg(&a.x[idx2(f + 1, pos, n)]);
-    }
-    v[m] = z;
-    if (m < H) xr[m] = z;
-  }
-  fft_lane<L, R, G, false>(v, sm, t, g, a.tw);
-#pragma unroll
-  for (int m = 0; m < R; ++m) v[m] = cmul(v[m], __ldg(&a.sym[t + m * T]));
-  fft_lane<L, R, G, true>(v, sm, t, g, a.tw);
-
-  double acc = 0.0;
-#pragma unroll
-  for (int m = 0; m < H; ++m) {
-    const int pos = t + m * T;
-    if (pos >= n) continue;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const long fh = f + h;
-      if (fh >= F) continue;
-      const double xv = h ? xr[m].y : xr[m].x;
-      const double tv = h ? v[m].y : v[m].x;
-      double val = a.scale * tv;
-      if (a.tkind == 1) {
-        const int k = (int)(fh / a.n1);
-        double nb = 0.0;
-        if (a.tdir < 0 && k >= 1) nb = __ldg(&a.x[idx2(fh - a.n1, pos, n)]);
-        if (a.tdir > 0 && k + 1 < a.nt) nb = __ldg(&a.x[idx2(fh + a.n1, pos, n)]);
-        val += a.tc0 * xv + a.tc1 * nb;
-      }
-      const size_t o = idx2(fh, pos, n);
-      if constexpr (MODE == 0) {
-        a.out[o] = val;
-      } else {
-        const double q = __ldg(&a.vp[o]) + val;
-        if (a.q_out) a.q_out[o] = q;
-        if (a.r) {
-          const double alpha = *a.a_num / *a.a_den;
-          const double rn = a.r[o] - alpha * q;
-          a.r[o] = rn;
-          acc += rn * rn;
-        }
-      }
-    }
-  }
-  if constexpr (MODE == 1) {
-    if (a.r) {
-      double vv[1] = {acc};
-      block_reduce<RED_SUM, 1>(vv, scratch);
-      grid_finalize<RED_SUM, 1>(vv, a.red, scratch);
-    }
-  }
-}
-
-// ================================================================ columns
-// Column pass along an axis of length n with inner stride C, outer count O:
-// element (o, pos, c) at o*n*C + pos*C + c.
-//   MODE 0 (acc): out = acc + scale * T x            (acc may alias out)
-//   MODE 2 (S mid, axis x1): Bp = u + scale*T p; w = Bp * inv_m2[o];
-//        vp = scale * T w + a1[o] p; reduce sum(a1 p^2 + w Bp)
-struct ColArgs {
-  const double* x;
-  const double* acc;
-  double* out;
-  double* w;
-  int O, n, C;
-  const double2* sym;
-  const double2* tw;
-  double scale;
-  const double* inv_m2;
-  const double* a1;
-  RedSlot red;
-};
-
-template <int L>
-__device__ __forceinline__ void col_load(const double* __restrict__ base, int n, int C, long c, int t,
-                                         double2 (&v)[Cfg<L>::R], int H) {
-  constexpr int R = Cfg<L>::R, T = Cfg<L>::T;
-  const bool pair = (c + 1 < C) && ((C & 1) == 0);
-#pragma unroll
-  for (int m = 0; m < R; ++m) {
-    const int pos = t + m * T;
-    double2 z = make_double2(0.0, 0.0);
-    if (m < H && pos < n && c < C) {
-      const double* p = base + (size_t)pos * C + c;
-      if (pair) {
-        z = __ldg(reinterpret_cast<const double2*>(p));
-      } else {
-        z.x = __ldg(p);
-        if (c + 1 < C) z.y = __ldg(p + 1);
-      }
-    }
-    v[m] = z;
-  }
-}
-
-__device__ __forceinline__ void col_store(double* base, int pos, int C, long c, double2 val) {
-  double* p = base + (size_t)pos * C + c;
-  if ((c + 1 < C) && ((C & 1) == 0)) {
-    *reinterpret_cast<double2*>(p) = val;
-  } else {
-    p[0] = val.x;
-    if (c + 1 < C) p[1] = val.y;
-  }
-}
-
-template <int L, int MODE>
-__global__ void __launch_bounds__(Cfg<L>::THREADS) k_col(ColArgs a) {
-  using Cf = Cfg<L>;
-  constexpr int R = Cf::R, T = Cf::T, G = Cf::G, H = (R + 1) / 2;
-  extern __shared__ double2 sm[];
-  __shared__ double scratch[32];
-  const int g = threadIdx.x % G, t = threadIdx.x / G;
-  const int o = blockIdx.y;
-  const long c = ((long)blockIdx.x * G + g) * 2;
-  const int n = a.n, C = a.C;
-  const size_t base = (size_t)o * n * C;
-  double2 v[R];
-  double2 keep[H];
-  col_load<L>(a.x + base, n, C, c, t, v, H);
-#pragma unroll
-  for (int m = 0; m < H; ++m) keep[m] = v[m];
-  fft_lane<L, R, G, false>(v, sm, t, g, a.tw);
-#pragma unroll
-  for (int m = 0; m < R; ++m) v[m] = cmul(v[m], __ldg(&a.sym[t + m * T]));
-  fft_lane<L, R, G, true>(v, sm, t, g, a.tw);
-
-  if constexpr (MODE == 0) {
-#pragma unroll
-    for (int m = 0; m < H; ++m) {
-      const int pos = t + m * T;
-      if (pos >= n || c >= C) continue;
-      double2 acc = make_double2(0.0, 0.0);
-      if (a.acc) {
-        const double* p = a.acc + base + (size_t)pos * C + c;
-        acc.x = p[0];
-        if (c + 1 < C) acc.y = p[1];
-      }
-      col_store(a.out + base, pos, C, c, make_double2(acc.x + a.scale * v[m].x, acc.y + a.scale * v[m].y));
-    }
-  } else {
-    // S mid pass: u is a.acc, w -> a.w, vp -> a.out
-    const double im2 = a.inv_m2[o], a1 = a.a1[o];
-    double e = 0.0;
-    double2 u[H];
-    double2 zero2 = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int m = 0; m < H; ++m) {
-      const int pos = t + m * T;
-      u[m] = zero2;
-      if (pos < n && c < C) {
-        const double* p = a.acc + base + (size_t)pos * C + c;
-        u[m].x = p[0];
-        if (c + 1 < C) u[m].y = p[1];
-      }
-    }
-#pragma unroll
-    for (int m = 0; m < R; ++m) {
-      const int pos = t + m * T;
-      if (m < H && pos < n && c < C) {
-        const double bx = u[m].x + a.scale * v[m].x;
-        const double by = u[m].y + a.scale * v[m].y;
-        const double wx = bx * im2, wy = (c + 1 < C) ? by * im2 : 0.0;
-        e += a1 * keep[m].x * keep[m].x + wx * bx;
-        if (c + 1 < C) e += a1 * keep[m].y * keep[m].y + wy * by;
-        col_store(a.w + base, pos, C, c, make_double2(wx, wy));
-        v[m] = make_double2(wx, wy);
-      } else {
-        v[m] = zero2;
-      }
-    }
-    fft_lane<L, R, G, false>(v, sm, t, g, a.tw);
-#pragma unroll
-    for (int m = 0; m < R; ++m) v[m] = cmul(v[m], __ldg(&a.sym[t + m * T]));
-    fft_lane<L, R, G, true>(v, sm, t, g, a.tw);
-#pragma unroll
-    for (int m = 0; m < H; ++m) {
-      const int pos = t + m * T;
-      if (pos >= n || c >= C) continue;
-      col_store(a.out + base, pos, C, c,
-                make_double2(a.scale * v[m].x + a1 * keep[m].x, a.scale * v[m].y + a1 * keep[m].y));
-    }
-    double vv[1] = {e};
-    block_reduce<RED_SUM, 1>(vv, scratch);
-    grid_finalize<RED_SUM, 1>(vv, a.red, scratch);
-  }
-}
-
-// ============================================================== Hartley
-// Real Hartley transform H[f] = sum_j x_j cas(2 pi j f / N) of two real
-// fibres packed as a + i b into one complex FFT (fdg_fft.cuh hartley_split).
-// For the circulant preconditioner the multiplier lambda_S is even in every
-// axis (spatial T. Chan eigenvalues are real and even; |conj(l_t) - s| =
-// |l_t - s| for real s), so F^-1 D F == H^-1 D H axis by axis: all three
-// passes stay real (N doubles in, N doubles out), see DESIGN.md.
-template <int N>
-__global__ void __launch_bounds__(Cfg<N>::THREADS) k_hartley_row(const double* in, double* out, int F,
-                                                                 const double2* tw, const double* rdot,
-                                                                 RedSlot red) {
-  using Cf = Cfg<N>;
-  constexpr int R = Cf::R, T = Cf::T, G = Cf::G;
-  extern __shared__ double2 sm[];
-  __shared__ double scratch[32];
-  const int g = threadIdx.x % G, t = threadIdx.x / G;
-  const long f = ((long)blockIdx.x * G + g) * 2;
-  const bool va = f < F, vb = f + 1 < F;
-  double2 v[R], w[R];
-#pragma unroll
-  for (int m = 0; m < R; ++m) {
-    const int pos = t + m * T;
-    v[m].x = va ? __ldg(&in[idx2(f, pos, N)]) : 0.0;
-    v[m].y = vb ? __ldg(&in[idx2(f + 1, pos, N)]) : 0.0;
-  }
-  fft_lane<N, R, G, false>(v, sm, t, g, tw);
-  mirror_lane<N, R, G>(v, w, sm, t, g);
-  double acc = 0.0;
-#pragma unroll
-  for (int m = 0; m < R; ++m) {
-    const int pos = t + m * T;
-    const double2 h = hartley_split(v[m], w[m]);
-    if (va) {
-      out[idx2(f, pos, N)] = h.x;
-      if (rdot) acc += __ldg(&rdot[idx2(f, pos, N)]) * h.x;
-    }
-    if (vb) {
-      out[idx2(f + 1, pos, N)] = h.y;
-      if (rdot) acc += __ldg(&rdot[idx2(f + 1, pos, N)]) * h.y;
-    }
-  }
-  if (rdot) {
-    double vv[1] = {acc};
-    block_reduce<RED_SUM, 1>(vv, scratch);
-    grid_finalize<RED_SUM, 1>(vv, red, scratch);
-  }
-}
-
-template <int N>
-__global__ void __launch_bounds__(Cfg<N>::THREADS) k_hartley_col(double* data, int C, const double2* tw) {
-  using Cf = Cfg<N>;
-  constexpr int R = Cf::R, T = Cf::T, G = Cf::G;
-  extern __shared__ double2 sm[];
-  const int g = threadIdx.x % G, t = threadIdx.x / G;
-  const long c = ((long)blockIdx.x * G + g) * 2;
-  const size_t base = (size_t)blockIdx.y * N * C;
-  double2 v[R], w[R];
-  col_load<N>(data + base, N, C, c, t, v, R);
-  fft_lane<N, R, G, false>(v, sm, t, g, tw);
-  mirror_lane<N, R, G>(v, w, sm, t, g);
-#pragma unroll
-  for (int m = 0; m < R; ++m) {
-    const int pos = t + m * T;
-    if (c < C) col_store(data + base, pos, C, c, hartley_split(v[m], w[m]));
-  }
-}
-
-// t pass of the preconditioner: Hartley along t, divide by lambda_S (computed
-// in registers from the 1-D eigenvalues, circulant.cpp:28-41, 76-90) and by
-// N (circulant.cpp:62-64), Hartley along t again.
-template <int N>
-__global__ void __launch_bounds__(Cfg<N>::THREADS) k_t_filter(double* data, PcTables pt) {
-  using Cf = Cfg<N>;
-  constexpr int R = Cf::R, T = Cf::T, G = Cf::G;
-  extern __shared__ double2 sm[];
-  const int g = threadIdx.x % G, t = threadIdx.x / G;
-  const int C = pt.n1 * pt.n2;
-  const long c = ((long)blockIdx.x * G + g) * 2;
-  double2 v[R], w[R];
-  col_load<N>(data, N, C, c, t, v, R);
-  fft_lane<N, R, G, false>(v, sm, t, g, pt.tw_t);
-  mirror_lane<N, R, G>(v, w, sm, t, g);
-  // spatial eigenvalue sums of the two packed columns
-  double2 sa = make_double2(0.0, 0.0), sb = make_double2(0.0, 0.0);
-  if (c < C) {
-    const int i = (int)(c / pt.n2), j = (int)(c % pt.n2);
-    const double2 l1 = __ldg(&pt.lam_1[i]), l2 = __ldg(&pt.lam_2[j]);
-    sa = make_double2(l1.x + l2.x, l1.y + l2.y);
-  }
-  if (c + 1 < C) {
-    const int i = (int)((c + 1) / pt.n2), j = (int)((c + 1) % pt.n2);
-    const double2 l1 = __ldg(&pt.lam_1[i]), l2 = __ldg(&pt.lam_2[j]);
-    sb = make_double2(l1.x + l2.x, l1.y + l2.y);
-  }
-#pragma unroll
-  for (int m = 0; m < R; ++m) {
-    const int k = t + m * T;
-    const double2 h = hartley_split(v[m], w[m]);
-    const double2 lt = __ldg(&pt.lam_t[k]);
-    const double bax = pt.psi * (lt.x - sa.x), bay = pt.psi * (lt.y - sa.y);
-    const double bbx = pt.psi * (lt.x - sb.x), bby = pt.psi * (lt.y - sb.y);
-    const double lsa = pt.base + (bax * bax + bay * bay) * pt.inv_m2;
-    const double lsb = pt.base + (bbx * bbx + bby * bby) * pt.inv_m2;
-    v[m] = make_double2(h.x / lsa * pt.inv_total, h.y / lsb * pt.inv_total);
-  }
-  fft_lane<N, R, G, false>(v, sm, t, g, pt.tw_t);
-  mirror_lane<N, R, G>(v, w, sm, t, g);
-#pragma unroll
-  for (int m = 0; m < R; ++m) {
-    const int pos = t + m * T;
-    if (c < C) col_store(data, pos, C, c, hartley_split(v[m], w[m]));
-  }
-}
 
 // ============================================================ elementwise
 namespace {
@@ -529,17 +174,33 @@ __global__ void k_objective(const double* y, const double* ybar, const double* v
 // ================================================================ dispatch
 #define FDG_POW2_CASES(X) X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048)
 
-// Opt in to > 48 KB dynamic shared memory once per kernel instantiation.
+// Opt in to > 48 KB dynamic shared memory and size the persistent grid
+// (resident CTAs x SMs) once per kernel instantiation and device.
+struct LaunchShape {
+  int device = -1;
+  int grid = 0;
+};
+
 template <auto K>
-static cudaError_t prep(size_t smem) {
-  static int done_device = -1;
+static cudaError_t prep(size_t smem, int threads, int& grid_cap) {
+  static LaunchShape ls;
   int dev = 0;
-  cudaGetDevice(&dev);
-  if (done_device != dev && smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (ls.device != dev) {
+    if (smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    int per_sm = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K, threads, smem);
     if (e != cudaSuccess) return e;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    ls.grid = (per_sm < 1 ? 1 : per_sm) * sms;
+    ls.device = dev;
   }
-  done_device = dev;
+  grid_cap = ls.grid;
   return cudaSuccess;
 }
 
@@ -547,21 +208,29 @@ static inline void count(LaunchCounter* lc, unsigned long long k = 1) {
   if (lc) lc->count += k;
 }
 
-static int pow2_ceil(long v) {
-  int L = 1;
-  while (L < v) L <<= 1;
-  return L;
+static inline unsigned clamp_grid(long tiles, int cap) {
+  return (unsigned)(tiles < cap ? (tiles < 1 ? 1 : tiles) : cap);
+}
+
+template <int L, int MODE, bool STAGE>
+static cudaError_t run_row_full(cudaStream_t st, const RowArgs& a) {
+  using Cf = Cfg<L>;
+  using RC = RowCfg<L, MODE, STAGE>;
+  int cap = 0;
+  cudaError_t e = prep<k_row<L, MODE, STAGE>>(RC::SMEM, Cf::THREADS, cap);
+  if (e != cudaSuccess) return e;
+  const long F = (long)a.nt * a.n1;
+  k_row<L, MODE, STAGE><<<clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, RC::SMEM, st>>>(a);
+  return cudaGetLastError();
 }
 
 template <int L, int MODE>
 static cudaError_t run_row(cudaStream_t st, const RowArgs& a) {
-  using Cf = Cfg<L>;
-  const long F = (long)a.nt * a.n1;
-  const unsigned grid = (unsigned)((F + 2 * Cf::G - 1) / (2 * Cf::G));
-  cudaError_t e = prep<k_row<L, MODE>>(Cf::SMEM);
-  if (e != cudaSuccess) return e;
-  k_row<L, MODE><<<grid, Cf::THREADS, Cf::SMEM, st>>>(a);
-  return cudaGetLastError();
+  // staged full tiles: n == L/2 and tiles of 2G fibres inside one time slice
+  if constexpr (L >= 16) {
+    if (2 * a.n == L && a.n1 % (2 * Cfg<L>::G) == 0) return run_row_full<L, MODE, true>(st, a);
+  }
+  return run_row_full<L, MODE, false>(st, a);
 }
 
 template <int MODE>
@@ -575,14 +244,21 @@ static cudaError_t dispatch_row(cudaStream_t st, int L, const RowArgs& a) {
   }
 }
 
+template <int L, int MODE, bool FULL>
+static cudaError_t run_col_full(cudaStream_t st, const ColArgs& a) {
+  using Cf = Cfg<L>;
+  int cap = 0;
+  cudaError_t e = prep<k_col<L, MODE, FULL>>(Cf::SMEM, Cf::THREADS, cap);
+  if (e != cudaSuccess) return e;
+  const long tiles = (long)a.O * ((a.C + 2 * Cf::G - 1) / (2 * Cf::G));
+  k_col<L, MODE, FULL><<<clamp_grid(tiles, cap), Cf::THREADS, Cf::SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
 template <int L, int MODE>
 static cudaError_t run_col(cudaStream_t st, const ColArgs& a) {
-  using Cf = Cfg<L>;
-  dim3 grid((unsigned)((a.C + 2 * Cf::G - 1) / (2 * Cf::G)), (unsigned)a.O);
-  cudaError_t e = prep<k_col<L, MODE>>(Cf::SMEM);
-  if (e != cudaSuccess) return e;
-  k_col<L, MODE><<<grid, Cf::THREADS, Cf::SMEM, st>>>(a);
-  return cudaGetLastError();
+  if (2 * a.n == L && a.C % (2 * Cfg<L>::G) == 0) return run_col_full<L, MODE, true>(st, a);
+  return run_col_full<L, MODE, false>(st, a);
 }
 
 template <int MODE>
@@ -609,7 +285,7 @@ cudaError_t launch_row_apply(cudaStream_t st, LaunchCounter* lc, const double* x
   a.tw = s2.tw;
   a.scale = scale;
   a.tkind = tf.kind == 1 ? 1 : 0;
-  a.tc0 = psi * tf.c0;
+  a.tc0 = 0.0;  // folded into the x2 symbol (fdg_api.cu ax2s)
   a.tc1 = psi * tf.c1;
   a.tdir = adjoint ? +1 : -1;
   count(lc);
@@ -632,7 +308,7 @@ cudaError_t launch_row_s_out(cudaStream_t st, LaunchCounter* lc, const double* w
   a.tw = s2.tw;
   a.scale = scale;
   a.tkind = tf.kind == 1 ? 1 : 0;
-  a.tc0 = psi * tf.c0;
+  a.tc0 = 0.0;  // folded into the x2 symbol (fdg_api.cu ax2s)
   a.tc1 = psi * tf.c1;
   a.tdir = +1;
   a.a_num = alpha_num;
@@ -683,31 +359,55 @@ template <int N>
 static cudaError_t run_hrow(cudaStream_t st, const double* in, double* out, int F, const double2* tw,
                             const double* rdot, RedSlot red) {
   using Cf = Cfg<N>;
-  const unsigned grid = (unsigned)((F + 2 * Cf::G - 1) / (2 * Cf::G));
-  cudaError_t e = prep<k_hartley_row<N>>(Cf::SMEM);
-  if (e != cudaSuccess) return e;
-  k_hartley_row<N><<<grid, Cf::THREADS, Cf::SMEM, st>>>(in, out, F, tw, rdot, red);
+  int cap = 0;
+  const long tiles = (F + 2 * Cf::G - 1) / (2 * Cf::G);
+  cudaError_t e;
+  if (F % (2 * Cf::G) == 0) {
+    e = prep<k_hartley_row<N, true>>(Cf::SMEM, Cf::THREADS, cap);
+    if (e != cudaSuccess) return e;
+    k_hartley_row<N, true><<<clamp_grid(tiles, cap), Cf::THREADS, Cf::SMEM, st>>>(in, out, F, tw, rdot, red);
+  } else {
+    e = prep<k_hartley_row<N, false>>(Cf::SMEM, Cf::THREADS, cap);
+    if (e != cudaSuccess) return e;
+    k_hartley_row<N, false><<<clamp_grid(tiles, cap), Cf::THREADS, Cf::SMEM, st>>>(in, out, F, tw, rdot, red);
+  }
   return cudaGetLastError();
 }
 
 template <int N>
 static cudaError_t run_hcol(cudaStream_t st, double* data, int O, int C, const double2* tw) {
   using Cf = Cfg<N>;
-  dim3 grid((unsigned)((C + 2 * Cf::G - 1) / (2 * Cf::G)), (unsigned)O);
-  cudaError_t e = prep<k_hartley_col<N>>(Cf::SMEM);
-  if (e != cudaSuccess) return e;
-  k_hartley_col<N><<<grid, Cf::THREADS, Cf::SMEM, st>>>(data, C, tw);
+  int cap = 0;
+  const long tiles = (long)O * ((C + 2 * Cf::G - 1) / (2 * Cf::G));
+  cudaError_t e;
+  if (C % (2 * Cf::G) == 0) {
+    e = prep<k_hartley_col<N, true>>(Cf::SMEM, Cf::THREADS, cap);
+    if (e != cudaSuccess) return e;
+    k_hartley_col<N, true><<<clamp_grid(tiles, cap), Cf::THREADS, Cf::SMEM, st>>>(data, O, C, tw);
+  } else {
+    e = prep<k_hartley_col<N, false>>(Cf::SMEM, Cf::THREADS, cap);
+    if (e != cudaSuccess) return e;
+    k_hartley_col<N, false><<<clamp_grid(tiles, cap), Cf::THREADS, Cf::SMEM, st>>>(data, O, C, tw);
+  }
   return cudaGetLastError();
 }
 
 template <int N>
 static cudaError_t run_tf(cudaStream_t st, double* data, const PcTables& pt) {
   using Cf = Cfg<N>;
+  int cap = 0;
   const long C = (long)pt.n1 * pt.n2;
-  const unsigned grid = (unsigned)((C + 2 * Cf::G - 1) / (2 * Cf::G));
-  cudaError_t e = prep<k_t_filter<N>>(Cf::SMEM);
-  if (e != cudaSuccess) return e;
-  k_t_filter<N><<<grid, Cf::THREADS, Cf::SMEM, st>>>(data, pt);
+  const long tiles = (C + 2 * Cf::G - 1) / (2 * Cf::G);
+  cudaError_t e;
+  if (C % (2 * Cf::G) == 0) {
+    e = prep<k_t_filter<N, true>>(Cf::SMEM, Cf::THREADS, cap);
+    if (e != cudaSuccess) return e;
+    k_t_filter<N, true><<<clamp_grid(tiles, cap), Cf::THREADS, Cf::SMEM, st>>>(data, pt);
+  } else {
+    e = prep<k_t_filter<N, false>>(Cf::SMEM, Cf::THREADS, cap);
+    if (e != cudaSuccess) return e;
+    k_t_filter<N, false><<<clamp_grid(tiles, cap), Cf::THREADS, Cf::SMEM, st>>>(data, pt);
+  }
   return cudaGetLastError();
 }
 

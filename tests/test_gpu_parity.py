@@ -52,7 +52,8 @@ def test_operator_golden(gpu_ctx, ref, golden, n):
 
 
 @pytest.mark.parametrize("shape", [(4, 8, 16), (16, 8, 4), (3, 5, 7), (32, 64, 64), (8, 128, 32),
-                                   (2, 256, 256), (1, 33, 47)])
+                                   (2, 256, 256), (1, 33, 47), (2, 16, 512), (2, 512, 16),
+                                   (2, 8, 1024), (2, 1024, 8), (2, 300, 700)])
 def test_operator_noncube_vs_port(gpu_ctx, port, shape):
     """Non-cube shapes (BASELINE C1/C3/C4 structure) against the generalized
     C restatement, anisotropic orders and diffusion coefficients."""
@@ -195,3 +196,37 @@ def test_admm_five_steps_golden(gpu_ctx, ref, golden, n):
     for f in ("y", "v", "p"):
         assert rel(drv.get(f), golden[f"ie{n}_after5_{f}"]) < 1e-8
     assert abs(drv.objective() - golden[f"ie{n}_after5_obj"][0]) <= 1e-8 * abs(golden[f"ie{n}_after5_obj"][0])
+
+
+@pytest.mark.parametrize("shape", [(4, 16, 256), (4, 8, 512), (2, 16, 64), (2, 4, 1024)])
+def test_pcg_noncube_vs_port(gpu_ctx, port, shape):
+    """PCG on the ADMM normal equations for shapes that select the staged
+    row kernels (tiles inside one slice) and the L >= 1024 single-buffer
+    kernels, against the generalized C restatement."""
+    from oracle import Shape, baseline_problem
+    from oracle.pyoracle import PortAdmm
+    from paper_1907_13428_b200 import AdmmConfig, AdmmDriver, assemble_precond
+    c = baseline_problem("C3", Shape(*shape))
+    pop = port.op(shape, c["time"], c["r1"], c["r2"], c["psi"])
+    ppc = pop.assemble_precond(1.0, 1.0, c["gamma"])
+    rng = np.random.default_rng(11)
+    yb = rng.standard_normal(pop.size)
+    padm = PortAdmm(port, pop, ppc, c["gamma"], 1.0, 1.0, y_lo=c["y"][0], y_hi=c["y"][1],
+                    u_lo=c["u"][0], u_hi=c["u"][1], tol_primal=1e-6, max_inner=400,
+                    fixed_tol=1e-8, ybar=yb)
+    op = gpu_op(gpu_ctx, c["time"], c["r1"], c["r2"], c["psi"])
+    pc = assemble_precond(op, 1.0, 1.0, c["gamma"])
+    cfg = AdmmConfig(delta=1.0, rho=1.0, tol_primal=1e-6, max_inner=400, fixed_krylov_tol=1e-8)
+    drv = AdmmDriver(op, pc, c["gamma"], cfg, y_lo=c["y"][0], y_hi=c["y"][1], u_lo=c["u"][0],
+                     u_hi=c["u"][1], ybar=yb)
+    x = rng.standard_normal(pop.size)
+    assert rel(drv.apply_S(x), padm.apply_S(x)) < OP_TOL
+    rhs = padm.build_rhs()[0]
+    assert rel(drv.build_rhs()[0], rhs) < OP_TOL
+    y_cpu, r_cpu = padm.pcg(rhs, tol=1e-8, max_inner=400)
+    y_gpu, r_gpu = drv.pcg(rhs, tol=1e-8, max_inner=400)
+    assert r_gpu.converged and abs(r_gpu.iterations - r_cpu["iterations"]) <= 1
+    assert rel(y_gpu, y_cpu) < 1e-7
+    for _ in range(2):
+        g, cpu = drv.step(), padm.step()
+        assert abs(g.inner_iters - cpu["inner_iters"]) <= 1
