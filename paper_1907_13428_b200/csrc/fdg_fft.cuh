@@ -175,14 +175,28 @@ struct Ex {
   double2* buf1;
   int k;
   __device__ __forceinline__ double2* next() {
-    // single buffer: every thread must have finished reading the previous
-    // exchange before anyone scatters the next one (write-after-read)
-    if (buf0 == buf1) __syncthreads();
     double2* p = k ? buf1 : buf0;
     k ^= 1;
     return p;
   }
+  __device__ __forceinline__ bool single() const { return buf0 == buf1; }
 };
+
+// Barrier of one exchange.  Lane-interleaved layout (0): the whole CTA shares
+// every smem row -> __syncthreads.  Lane-major layout (1): each lane owns a
+// private region, so only the lane's T threads synchronize: __syncwarp when a
+// lane is (part of) one warp, a named barrier (id 1 + lane) otherwise.  Lanes
+// then run their FFTs independently instead of in CTA-wide lock step.
+template <int LAYOUT, int T>
+__device__ __forceinline__ void lane_sync(int g) {
+  if constexpr (LAYOUT == 0) {
+    __syncthreads();
+  } else if constexpr (T <= 32) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + g), "n"(T) : "memory");
+  }
+}
 
 // Registers per thread (= radix bound) used for a transform of length N;
 // shared by the kernels (Cfg) and the host twiddle-table builder.
@@ -218,16 +232,27 @@ struct Stockham {
     for (int s = 0; s < S; ++s) {
       const int b = t + s * T;  // butterfly index in [0, N/Rp)
       if constexpr (Ns > 1) {
+        // Load the power-of-two twiddles w^1, w^2, w^4(, w^8) and form the
+        // others as products (3 of 7 loads for radix 8): the shared-memory
+        // pipe, not FP64, is the busiest unit of these kernels.
         const double2* tw = ptw + OFF + (b & (Ns - 1));
+        double2 wt[Rp];
 #pragma unroll
         for (int r = 1; r < Rp; ++r) {
-          const double2 w = tw[(r - 1) * Ns];
-          v[s + r * S] = INV ? cmulc(v[s + r * S], w) : cmul(v[s + r * S], w);
+          if ((r & (r - 1)) == 0) {
+            wt[r] = tw[(r - 1) * Ns];
+          } else {
+            const int lo = r & -r;
+            wt[r] = cmul(wt[lo], wt[r - lo]);
+          }
         }
+#pragma unroll
+        for (int r = 1; r < Rp; ++r) v[s + r * S] = INV ? cmulc(v[s + r * S], wt[r]) : cmul(v[s + r * S], wt[r]);
       }
       Dft<Rp, INV>::run(v, s, S);
     }
     if constexpr (!LAST) {
+      if (ex.single()) lane_sync<LAYOUT, T>(g);  // write-after-read on the single buffer
       double2* sm = ex.next();
       // scatter: out[(b/Ns)*Ns*Rp + b%Ns + r*Ns] = v[s + r*S]
 #pragma unroll
@@ -237,7 +262,7 @@ struct Stockham {
 #pragma unroll
         for (int r = 0; r < Rp; ++r) sm[slot<LAYOUT, N, G>(base + r * Ns, g)] = v[s + r * S];
       }
-      __syncthreads();
+      lane_sync<LAYOUT, T>(g);
 #pragma unroll
       for (int m = 0; m < R; ++m) v[m] = sm[slot<LAYOUT, N, G>(t + m * T, g)];
       Stockham<N, R, G, INV, Ns * Rp, LAYOUT, NEXT_OFF>::run(v, ex, t, g, ptw);
@@ -246,7 +271,7 @@ struct Stockham {
 };
 
 // Full FFT of length N on the lane; x[t + m*T] in v[m] before and after.
-// Every thread of the CTA must call it (it contains __syncthreads()).
+// Every thread of the lane (LAYOUT 1) / CTA (LAYOUT 0) must call it.
 template <int N, int R, int G, bool INV, int LAYOUT = 0>
 __device__ __forceinline__ void fft_lane(double2 (&v)[R], Ex& ex, int t, int g, const double2* tw) {
   if constexpr (N == 1) {
@@ -257,14 +282,15 @@ __device__ __forceinline__ void fft_lane(double2 (&v)[R], Ex& ex, int t, int g, 
 }
 
 // Exchange helper: value at position (N - pos) mod N for every register
-// (used by the Hartley post-processing).  One __syncthreads().
+// (used by the Hartley post-processing).  One barrier (lane_sync).
 template <int N, int R, int G, int LAYOUT = 0>
 __device__ __forceinline__ void mirror_lane(const double2 (&v)[R], double2 (&w)[R], Ex& ex, int t, int g) {
   constexpr int T = N / R;
+  if (ex.single()) lane_sync<LAYOUT, T>(g);
   double2* sm = ex.next();
 #pragma unroll
   for (int m = 0; m < R; ++m) sm[slot<LAYOUT, N, G>(t + m * T, g)] = v[m];
-  __syncthreads();
+  lane_sync<LAYOUT, T>(g);
 #pragma unroll
   for (int m = 0; m < R; ++m) {
     const int pos = t + m * T;
@@ -273,16 +299,35 @@ __device__ __forceinline__ void mirror_lane(const double2 (&v)[R], double2 (&w)[
   }
 }
 
-// Cooperative copy of a small global table into shared memory.
-__device__ __forceinline__ void load_table(double2* dst, const double2* __restrict__ src, int n) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(&src[i]);
-}
-
 // Two packed real sequences a + i b -> (Hartley(a), Hartley(b)) given
 // Z = FFT(a + i b): H_a[f] = (zr - zi + wr + wi)/2, H_b[f] = (zr + zi - wr + wi)/2
 // with W = Z[N - f].  Returned packed as H_a + i H_b.
 __device__ __forceinline__ double2 hartley_split(double2 z, double2 w) {
   return make_double2(0.5 * ((z.x - z.y) + (w.x + w.y)), 0.5 * ((z.x + z.y) - (w.x - w.y)));
 }
+
+// Hartley post-processing in place: v[m] <- hartley_split(v[m], V[N - pos])
+// (two packed real sequences -> their Hartley transforms), one exchange and
+// no second register array.
+template <int N, int R, int G, int LAYOUT = 0>
+__device__ __forceinline__ void hartley_lane(double2 (&v)[R], Ex& ex, int t, int g) {
+  constexpr int T = N / R;
+  if (ex.single()) lane_sync<LAYOUT, T>(g);
+  double2* sm = ex.next();
+#pragma unroll
+  for (int m = 0; m < R; ++m) sm[slot<LAYOUT, N, G>(t + m * T, g)] = v[m];
+  lane_sync<LAYOUT, T>(g);
+#pragma unroll
+  for (int m = 0; m < R; ++m) {
+    const int mp = (N - (t + m * T)) & (N - 1);
+    v[m] = hartley_split(v[m], sm[slot<LAYOUT, N, G>(mp, g)]);
+  }
+}
+
+// Cooperative copy of a small global table into shared memory.
+__device__ __forceinline__ void load_table(double2* dst, const double2* __restrict__ src, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = __ldg(&src[i]);
+}
+
 
 }  // namespace fdg

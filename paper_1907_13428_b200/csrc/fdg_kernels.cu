@@ -212,25 +212,25 @@ static inline unsigned clamp_grid(long tiles, int cap) {
   return (unsigned)(tiles < cap ? (tiles < 1 ? 1 : tiles) : cap);
 }
 
-template <int L, int MODE, bool STAGE>
-static cudaError_t run_row_full(cudaStream_t st, const RowArgs& a) {
+template <int L, int MODE, bool PF>
+static cudaError_t run_row_v(cudaStream_t st, const RowArgs& a) {
   using Cf = Cfg<L>;
-  using RC = RowCfg<L, MODE, STAGE>;
+  constexpr size_t SM = RowPlan<L, MODE, PF>::SMEM;
   int cap = 0;
-  cudaError_t e = prep<k_row<L, MODE, STAGE>>(RC::SMEM, Cf::THREADS, cap);
+  cudaError_t e = prep<k_row<L, MODE, PF>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
   const long F = (long)a.nt * a.n1;
-  k_row<L, MODE, STAGE><<<clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, RC::SMEM, st>>>(a);
+  k_row<L, MODE, PF><<<clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st>>>(a);
   return cudaGetLastError();
 }
 
 template <int L, int MODE>
 static cudaError_t run_row(cudaStream_t st, const RowArgs& a) {
-  // staged full tiles: n == L/2 and tiles of 2G fibres inside one time slice
-  if constexpr (L >= 16) {
-    if (2 * a.n == L && a.n1 % (2 * Cfg<L>::G) == 0) return run_row_full<L, MODE, true>(st, a);
+  // pipelined full tiles: n == L/2 and tiles of 2G fibres inside one slice
+  if constexpr (Cfg<L>::PF_OK) {
+    if (2 * a.n == L && a.n1 % (2 * Cfg<L>::G) == 0) return run_row_v<L, MODE, true>(st, a);
   }
-  return run_row_full<L, MODE, false>(st, a);
+  return run_row_v<L, MODE, false>(st, a);
 }
 
 template <int MODE>
@@ -244,21 +244,24 @@ static cudaError_t dispatch_row(cudaStream_t st, int L, const RowArgs& a) {
   }
 }
 
-template <int L, int MODE, bool FULL>
-static cudaError_t run_col_full(cudaStream_t st, const ColArgs& a) {
+template <int L, int MODE, bool PF>
+static cudaError_t run_col_v(cudaStream_t st, const ColArgs& a) {
   using Cf = Cfg<L>;
+  constexpr size_t SM = ColPlan<L, PF>::SMEM;
   int cap = 0;
-  cudaError_t e = prep<k_col<L, MODE, FULL>>(Cf::SMEM, Cf::THREADS, cap);
+  cudaError_t e = prep<k_col<L, MODE, PF>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
   const long tiles = (long)a.O * ((a.C + 2 * Cf::G - 1) / (2 * Cf::G));
-  k_col<L, MODE, FULL><<<clamp_grid(tiles, cap), Cf::THREADS, Cf::SMEM, st>>>(a);
+  k_col<L, MODE, PF><<<clamp_grid(tiles, cap), Cf::THREADS, SM, st>>>(a);
   return cudaGetLastError();
 }
 
 template <int L, int MODE>
 static cudaError_t run_col(cudaStream_t st, const ColArgs& a) {
-  if (2 * a.n == L && a.C % (2 * Cfg<L>::G) == 0) return run_col_full<L, MODE, true>(st, a);
-  return run_col_full<L, MODE, false>(st, a);
+  if constexpr (Cfg<L>::PF_OK) {
+    if (2 * a.n == L && a.C % (2 * Cfg<L>::G) == 0) return run_col_v<L, MODE, true>(st, a);
+  }
+  return run_col_v<L, MODE, false>(st, a);
 }
 
 template <int MODE>
@@ -355,60 +358,67 @@ cudaError_t launch_col_s_mid(cudaStream_t st, LaunchCounter* lc, const double* p
   return dispatch_col<2>(st, s1.L, a);
 }
 
+template <int N, bool PF>
+static cudaError_t run_hrow_v(cudaStream_t st, const double* in, double* out, int F, const double2* tw,
+                              const double* rdot, RedSlot red) {
+  using Cf = Cfg<N>;
+  constexpr size_t SM = HPlan<N, PF>::SMEM;
+  int cap = 0;
+  cudaError_t e = prep<k_hartley_row<N, PF>>(SM, Cf::THREADS, cap);
+  if (e != cudaSuccess) return e;
+  k_hartley_row<N, PF><<<clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st>>>(in, out, F, tw,
+                                                                                                      rdot, red);
+  return cudaGetLastError();
+}
+
 template <int N>
 static cudaError_t run_hrow(cudaStream_t st, const double* in, double* out, int F, const double2* tw,
                             const double* rdot, RedSlot red) {
-  using Cf = Cfg<N>;
-  int cap = 0;
-  const long tiles = (F + 2 * Cf::G - 1) / (2 * Cf::G);
-  cudaError_t e;
-  if (F % (2 * Cf::G) == 0) {
-    e = prep<k_hartley_row<N, true>>(Cf::SMEM, Cf::THREADS, cap);
-    if (e != cudaSuccess) return e;
-    k_hartley_row<N, true><<<clamp_grid(tiles, cap), Cf::THREADS, Cf::SMEM, st>>>(in, out, F, tw, rdot, red);
-  } else {
-    e = prep<k_hartley_row<N, false>>(Cf::SMEM, Cf::THREADS, cap);
-    if (e != cudaSuccess) return e;
-    k_hartley_row<N, false><<<clamp_grid(tiles, cap), Cf::THREADS, Cf::SMEM, st>>>(in, out, F, tw, rdot, red);
+  if constexpr (Cfg<N>::PF_OK) {
+    if (F % (2 * Cfg<N>::G) == 0) return run_hrow_v<N, true>(st, in, out, F, tw, rdot, red);
   }
+  return run_hrow_v<N, false>(st, in, out, F, tw, rdot, red);
+}
+
+template <int N, bool PF>
+static cudaError_t run_hcol_v(cudaStream_t st, double* data, int O, int C, const double2* tw) {
+  using Cf = Cfg<N>;
+  constexpr size_t SM = HPlan<N, PF>::SMEM;
+  int cap = 0;
+  cudaError_t e = prep<k_hartley_col<N, PF>>(SM, Cf::THREADS, cap);
+  if (e != cudaSuccess) return e;
+  const long tiles = (long)O * ((C + 2 * Cf::G - 1) / (2 * Cf::G));
+  k_hartley_col<N, PF><<<clamp_grid(tiles, cap), Cf::THREADS, SM, st>>>(data, O, C, tw);
   return cudaGetLastError();
 }
 
 template <int N>
 static cudaError_t run_hcol(cudaStream_t st, double* data, int O, int C, const double2* tw) {
-  using Cf = Cfg<N>;
-  int cap = 0;
-  const long tiles = (long)O * ((C + 2 * Cf::G - 1) / (2 * Cf::G));
-  cudaError_t e;
-  if (C % (2 * Cf::G) == 0) {
-    e = prep<k_hartley_col<N, true>>(Cf::SMEM, Cf::THREADS, cap);
-    if (e != cudaSuccess) return e;
-    k_hartley_col<N, true><<<clamp_grid(tiles, cap), Cf::THREADS, Cf::SMEM, st>>>(data, O, C, tw);
-  } else {
-    e = prep<k_hartley_col<N, false>>(Cf::SMEM, Cf::THREADS, cap);
-    if (e != cudaSuccess) return e;
-    k_hartley_col<N, false><<<clamp_grid(tiles, cap), Cf::THREADS, Cf::SMEM, st>>>(data, O, C, tw);
+  if constexpr (Cfg<N>::PF_OK) {
+    if (C % (2 * Cfg<N>::G) == 0) return run_hcol_v<N, true>(st, data, O, C, tw);
   }
+  return run_hcol_v<N, false>(st, data, O, C, tw);
+}
+
+template <int N, bool PF>
+static cudaError_t run_tf_v(cudaStream_t st, double* data, const PcTables& pt) {
+  using Cf = Cfg<N>;
+  constexpr size_t SM = HPlan<N, PF>::SMEM_T;
+  int cap = 0;
+  cudaError_t e = prep<k_t_filter<N, PF>>(SM, Cf::THREADS, cap);
+  if (e != cudaSuccess) return e;
+  const long C = (long)pt.n1 * pt.n2;
+  k_t_filter<N, PF><<<clamp_grid((C + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st>>>(data, pt);
   return cudaGetLastError();
 }
 
 template <int N>
 static cudaError_t run_tf(cudaStream_t st, double* data, const PcTables& pt) {
-  using Cf = Cfg<N>;
-  int cap = 0;
   const long C = (long)pt.n1 * pt.n2;
-  const long tiles = (C + 2 * Cf::G - 1) / (2 * Cf::G);
-  cudaError_t e;
-  if (C % (2 * Cf::G) == 0) {
-    e = prep<k_t_filter<N, true>>(Cf::SMEM, Cf::THREADS, cap);
-    if (e != cudaSuccess) return e;
-    k_t_filter<N, true><<<clamp_grid(tiles, cap), Cf::THREADS, Cf::SMEM, st>>>(data, pt);
-  } else {
-    e = prep<k_t_filter<N, false>>(Cf::SMEM, Cf::THREADS, cap);
-    if (e != cudaSuccess) return e;
-    k_t_filter<N, false><<<clamp_grid(tiles, cap), Cf::THREADS, Cf::SMEM, st>>>(data, pt);
+  if constexpr (Cfg<N>::PF_OK) {
+    if (C % (2 * Cfg<N>::G) == 0) return run_tf_v<N, true>(st, data, pt);
   }
-  return cudaGetLastError();
+  return run_tf_v<N, false>(st, data, pt);
 }
 
 #define FDG_POW2_CASES1(X) X(1) FDG_POW2_CASES(X)

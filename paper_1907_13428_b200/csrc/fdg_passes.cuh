@@ -2,9 +2,16 @@
 //
 // Every pass is one kernel over "tiles" of 2G fibres (two real fibres packed
 // as one complex FFT lane, G lanes per CTA).  CTAs are persistent (grid =
-// resident CTAs), stage the per-axis twiddle table and Toeplitz symbol in
-// shared memory once, and loop over tiles.  FULL = the tile needs no bounds
-// predicates (n == L/2 for Toeplitz embeddings, tile fully inside the array).
+// resident CTAs, 2 per SM), stage the per-axis twiddle table in shared memory
+// once and loop over tiles.
+//
+// Two variants per pass:
+//   PF = true  ("full tiles": n == L/2 for Toeplitz embeddings, tiles inside
+//              the array, L <= 512): software-pipelined.  While a CTA runs the
+//              FFTs of tile i, cp.async brings tile i+1's input (and tile i's
+//              epilogue operands) into shared memory, so neither the tile load
+//              nor the epilogue reads stall on HBM latency.
+//   PF = false (any shape): direct loads with bounds predicates.
 //
 // Reference: ConstraintOperator::apply_mode (toeplitz.cpp:124-172) — pack,
 // r2c, x symbol, c2r, unpack-accumulate — is one register-resident
@@ -22,7 +29,7 @@ namespace fdg {
 
 // Tile configuration for transform length L.
 //   R: complex values per thread, T = L/R threads per lane, G lanes per CTA
-//   (256 threads), DB: double-buffered exchanges, TS: tables in smem.
+//   (256 threads), DB: double-buffered exchanges, TS: twiddles in smem.
 template <int L>
 struct Cfg {
   static constexpr int R = fft_radix(L);
@@ -34,17 +41,25 @@ struct Cfg {
   static constexpr bool DB = L <= 512;
   static constexpr bool TS = L <= 1024;
   static constexpr size_t EXB = (size_t)L * G;  // double2 per exchange buffer
-  // exchange buffer(s) + twiddle table + symbol table
-  static constexpr size_t SMEM = sizeof(double2) * (EXB * (DB ? 2 : 1) + (TS ? 2 * (size_t)L : 0));
+  static constexpr bool PF_OK = L >= 16 && L <= 512;
 };
 
-template <int L, bool DB = Cfg<L>::DB>
+// Shared-memory plan: exchange buffer(s) | twiddles | extra table | staging.
+template <int L, bool DB, int EXTRA_TAB, int STAGE_DOUBLES>
+struct Plan {
+  using C = Cfg<L>;
+  static constexpr size_t EX = C::EXB * (DB ? 2 : 1);               // double2
+  static constexpr size_t TAB = (C::TS ? (size_t)L : 0) + EXTRA_TAB;  // double2
+  static constexpr size_t BYTES = sizeof(double2) * (EX + TAB) + sizeof(double) * (size_t)STAGE_DOUBLES;
+};
+
+template <int L, bool DB>
 struct Smem {
   Ex ex;
   const double2* tw;
-  const double2* sym;
-  double* stage;  // first byte after the tables (staging area, if any)
-  __device__ __forceinline__ Smem(double2* base, const double2* gtw, const double2* gsym) {
+  double2* tab;   // first double2 after the twiddles (extra table)
+  double* stage;  // staging area (after the extra table)
+  __device__ __forceinline__ Smem(double2* base, const double2* gtw, int extra_tab) {
     using C = Cfg<L>;
     ex.buf0 = base;
     ex.buf1 = DB ? base + C::EXB : base;
@@ -53,19 +68,12 @@ struct Smem {
     if constexpr (C::TS) {
       load_table(t, gtw, L);
       tw = t;
-      if (gsym) {
-        load_table(t + L, gsym, L);
-        sym = t + L;
-      } else {
-        sym = nullptr;
-      }
-      stage = reinterpret_cast<double*>(t + 2 * L);
-      __syncthreads();
+      t += L;
     } else {
       tw = gtw;
-      sym = gsym;
-      stage = reinterpret_cast<double*>(t);
     }
+    tab = t;
+    stage = reinterpret_cast<double*>(t + extra_tab);
   }
 };
 
@@ -76,19 +84,31 @@ __device__ __forceinline__ void cp_async16(void* dst_smem, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 // CTA-cooperative contiguous copy of `nd` doubles (nd even, 16-byte aligned).
-__device__ __forceinline__ void stage_copy(double* dst, const double* src, int nd) {
+__device__ __forceinline__ void stage_rows(double* dst, const double* src, int nd) {
   for (int i = 2 * threadIdx.x; i < nd; i += 2 * blockDim.x) cp_async16(dst + i, src + i);
 }
-
-__device__ __forceinline__ size_t idx2(size_t a, size_t b, size_t n) { return a * n + b; }
+// CTA-cooperative copy of a column tile: n positions x W doubles (W even),
+// source row stride C doubles -> dense [pos][W] in shared memory.
+template <int W>
+__device__ __forceinline__ void stage_cols(double* dst, const double* src, int n, int C) {
+  constexpr int CH = W / 2;  // 16-byte chunks per position
+  for (int i = threadIdx.x; i < n * CH; i += blockDim.x) {
+    const int pos = i / CH, j = i - pos * CH;
+    cp_async16(dst + pos * W + 2 * j, src + (size_t)pos * C + 2 * j);
+  }
+}
 
 // =================================================================== rows
 // Row pass along x2 (contiguous fibres of length n; embedding length L).
-//   MODE 0 (apply):  out = psi*time(x) + scale * T2 x
-//   MODE 1 (S out):  q = vp + psi*time^T(x) + scale * T2 x; q_out = q (opt);
+//   MODE 0 (apply):  out = scale * T2 x + psi c1 x_{k-+1}
+//   MODE 1 (S out):  q = vp + scale * T2 x + psi c1 x_{k+1}; q_out = q (opt);
 //                    r -= (num/den) q; reduce |r|^2
+// The stencil diagonal psi c0 x_k is folded into the x2 symbol on the host.
 struct RowArgs {
   const double* x;
   const double* vp;
@@ -107,33 +127,29 @@ struct RowArgs {
   RedSlot red;
 };
 
-// Row kernel variants: STAGE = full tiles (n == L/2, tiles of 2G fibres
-// inside one time slice) whose epilogue operands (time-stencil neighbour row,
-// vp, r) are copied to shared memory by cp.async at tile start and arrive
-// during the FFTs.  The stencil diagonal psi c0 x_k is folded into the x2
-// symbol on the host, so only the neighbour term psi c1 x_{k-+1} remains.
-template <int L, int MODE, bool STAGE>
-struct RowCfg {
+template <int L, int MODE, bool PF>
+struct RowPlan {
   using C = Cfg<L>;
-  static constexpr int NSTAGE = STAGE ? (MODE == 1 ? 3 : 1) : 0;
-  static constexpr bool DB = C::DB && !(STAGE && MODE == 1);
-  static constexpr size_t SMEM = sizeof(double2) * (C::EXB * (DB ? 2 : 1) + (C::TS ? 2 * (size_t)L : 0)) +
-                                 sizeof(double) * (size_t)NSTAGE * 2 * C::G * (L / 2);
+  static constexpr int TILE = PF ? 2 * C::G * (L / 2) : 0;  // doubles per staged operand
+  static constexpr int NEPI = PF ? (MODE == 1 ? 3 : 1) : 0;
+  static constexpr bool DB = C::DB && !(PF && MODE == 1);
+  using P = Plan<L, DB, 0, TILE * (1 + NEPI)>;
+  static constexpr size_t SMEM = P::BYTES;
 };
 
-template <int L, int MODE, bool STAGE>
+template <int L, int MODE, bool PF>
 __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_row(RowArgs a) {
   using C = Cfg<L>;
-  using RC = RowCfg<L, MODE, STAGE>;
+  using RP = RowPlan<L, MODE, PF>;
   constexpr int R = C::R, T = C::T, G = C::G, H = (R + 1) / 2;
-  constexpr bool FULL = STAGE;
-  constexpr int TILE = 2 * G * (L / 2);  // doubles per staged operand
+  constexpr int TILE = RP::TILE;
   extern __shared__ double2 smem_raw[];
   __shared__ double scratch[32];
-  Smem<L, RC::DB> S(smem_raw, a.tw, a.sym);
-  double* st_nb = S.stage;
-  double* st_vp = S.stage + TILE;
-  double* st_r = S.stage + 2 * TILE;
+  Smem<L, RP::DB> S(smem_raw, a.tw, 0);
+  double* st_in = S.stage;
+  double* st_nb = S.stage + TILE;
+  double* st_vp = S.stage + 2 * TILE;
+  double* st_r = S.stage + 3 * TILE;
   const int g = threadIdx.x / T, t = threadIdx.x % T;  // lane-major: coalesced rows
   const int F = a.nt * a.n1;
   const int ntiles = (F + 2 * G - 1) / (2 * G);
@@ -144,56 +160,73 @@ __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_row(RowArgs a
   }
   const ptrdiff_t noff = (ptrdiff_t)a.tdir * a.n1 * n;
   double acc = 0.0;
+  if constexpr (PF) {
+    if (blockIdx.x < ntiles) stage_rows(st_in, a.x + (size_t)blockIdx.x * 2 * G * n, TILE);
+    cp_async_commit();
+  }
+  __syncthreads();  // twiddle table
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int f0 = tile * 2 * G;
     const int f = f0 + 2 * g;
-    const bool va = FULL || f < F, vb = FULL || f + 1 < F;
+    const bool va = PF || f < F, vb = PF || f + 1 < F;
     const double* xa = a.x + (size_t)f * n;
+    double2 v[R];
     bool tile_nb = false;
-    if constexpr (STAGE) {
+    if constexpr (PF) {
+      cp_async_wait<0>();
+      __syncthreads();
+#pragma unroll
+      for (int m = 0; m < R; ++m) {
+        const int pos = t + m * T;
+        v[m] = m < H ? make_double2(st_in[(2 * g) * n + pos], st_in[(2 * g + 1) * n + pos])
+                     : make_double2(0.0, 0.0);
+      }
+      __syncthreads();  // st_in and the epilogue staging are free
       const int k = f0 / a.n1;  // whole tile in one slice
       tile_nb = a.tkind == 1 && (a.tdir < 0 ? k >= 1 : k + 1 < a.nt);
-      if (tile_nb) stage_copy(st_nb, a.x + (size_t)f0 * n + noff, TILE);
+      if (tile_nb) stage_rows(st_nb, a.x + (size_t)f0 * n + noff, TILE);
       if constexpr (MODE == 1) {
-        stage_copy(st_vp, a.vp + (size_t)f0 * n, TILE);
-        if (a.r) stage_copy(st_r, a.r + (size_t)f0 * n, TILE);
+        stage_rows(st_vp, a.vp + (size_t)f0 * n, TILE);
+        if (a.r) stage_rows(st_r, a.r + (size_t)f0 * n, TILE);
       }
-      cp_async_commit();
-    }
-    double2 v[R];
+      cp_async_commit();  // group E: this tile's epilogue operands
+      const int nxt = tile + gridDim.x;
+      if (nxt < ntiles) stage_rows(st_in, a.x + (size_t)nxt * 2 * G * n, TILE);
+      cp_async_commit();  // group I: next tile's input
+    } else {
 #pragma unroll
-    for (int m = 0; m < R; ++m) {
-      const int pos = t + m * T;
-      double2 z = make_double2(0.0, 0.0);
-      if (m < H && (FULL || pos < n)) {
-        if (va) z.x = __ldg(xa + pos);
-        if (vb) z.y = __ldg(xa + n + pos);
+      for (int m = 0; m < R; ++m) {
+        const int pos = t + m * T;
+        double2 z = make_double2(0.0, 0.0);
+        if (m < H && pos < n) {
+          if (va) z.x = __ldg(xa + pos);
+          if (vb) z.y = __ldg(xa + n + pos);
+        }
+        v[m] = z;
       }
-      v[m] = z;
     }
     fft_lane<L, R, G, false, 1>(v, S.ex, t, g, S.tw);
 #pragma unroll
-    for (int m = 0; m < R; ++m) v[m] = cmul(v[m], S.sym[t + m * T]);
+    for (int m = 0; m < R; ++m) v[m] = cmul(v[m], __ldg(&a.sym[t + m * T]));
     fft_lane<L, R, G, true, 1>(v, S.ex, t, g, S.tw);
 
-    if constexpr (STAGE) {
-      cp_async_wait_all();
+    if constexpr (PF) {
+      cp_async_wait<1>();  // group E landed (group I may still fly)
       __syncthreads();
     }
-    // generic path: per-fibre neighbour predicates
     const int ka = f / a.n1, kb = (f + 1) / a.n1;
     const bool nba = a.tkind == 1 && (a.tdir < 0 ? ka >= 1 : ka + 1 < a.nt);
     const bool nbb = a.tkind == 1 && (a.tdir < 0 ? kb >= 1 : kb + 1 < a.nt);
 #pragma unroll
     for (int m = 0; m < H; ++m) {
       const int pos = t + m * T;
-      if (!FULL && pos >= n) continue;
+      if (!PF && pos >= n) continue;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        if (!FULL && !(h ? vb : va)) continue;
-        const int sl = (2 * g + h) * n + pos;  // staged element (STAGE)
+        if (!PF && !(h ? vb : va)) continue;
+        const int sl = (2 * g + h) * n + pos;  // staged element
         double val = a.scale * (h ? v[m].y : v[m].x);
-        if constexpr (STAGE) {
+        if constexpr (PF) {
           if (tile_nb) val += a.tc1 * st_nb[sl];
         } else {
           if (h ? nbb : nba) val += a.tc1 * __ldg(xa + h * n + pos + noff);
@@ -202,17 +235,16 @@ __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_row(RowArgs a
         if constexpr (MODE == 0) {
           a.out[o] = val;
         } else {
-          const double q = (STAGE ? st_vp[sl] : __ldg(&a.vp[o])) + val;
+          const double q = (PF ? st_vp[sl] : __ldg(&a.vp[o])) + val;
           if (a.q_out) a.q_out[o] = q;
           if (a.r) {
-            const double rn = (STAGE ? st_r[sl] : a.r[o]) - alpha * q;
+            const double rn = (PF ? st_r[sl] : a.r[o]) - alpha * q;
             a.r[o] = rn;
             acc += rn * rn;
           }
         }
       }
     }
-    if constexpr (STAGE) __syncthreads();  // staging is rewritten by the next tile
   }
   if constexpr (MODE == 1) {
     if (a.r) {
@@ -259,62 +291,95 @@ __device__ __forceinline__ void col_put(double* p, int C, long c, double2 val) {
   }
 }
 
-template <int L, int MODE, bool FULL>
+template <int L, bool PF>
+struct ColPlan {
+  using C = Cfg<L>;
+  static constexpr int TILE = PF ? 2 * C::G * (L / 2) : 0;
+  using P = Plan<L, C::DB, 0, TILE>;
+  static constexpr size_t SMEM = P::BYTES;
+};
+
+template <int L, int MODE, bool PF>
 __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_col(ColArgs a) {
   using Cf = Cfg<L>;
   constexpr int R = Cf::R, T = Cf::T, G = Cf::G, H = (R + 1) / 2;
+  constexpr int W = 2 * G;  // columns per tile
   extern __shared__ double2 smem_raw[];
   __shared__ double scratch[32];
-  Smem<L> S(smem_raw, a.tw, a.sym);
+  Smem<L, Cf::DB> S(smem_raw, a.tw, 0);
+  double* st_in = S.stage;
   const int g = threadIdx.x % G, t = threadIdx.x / G;
   const int n = a.n, C = a.C;
-  const int ncb = (C + 2 * G - 1) / (2 * G);
+  const int ncb = (C + W - 1) / W;
   const int ntiles = ncb * a.O;
+  if constexpr (PF) {
+    if (blockIdx.x < ntiles) {
+      const int o = blockIdx.x / ncb;
+      stage_cols<W>(st_in, a.x + (size_t)o * n * C + (size_t)(blockIdx.x - o * ncb) * W, n, C);
+    }
+    cp_async_commit();
+  }
+  __syncthreads();  // twiddle table
   double e = 0.0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int o = tile / ncb;
     const long c = (long)((tile - o * ncb) * G + g) * 2;
-    const bool vc = FULL || c < C;
+    const bool vc = PF || c < C;
     const size_t base = (size_t)o * n * C + c;
     double2 v[R];
+    if constexpr (PF) {
+      cp_async_wait<0>();
+      __syncthreads();
 #pragma unroll
-    for (int m = 0; m < R; ++m) {
-      const int pos = t + m * T;
-      v[m] = (m < H && (FULL || pos < n) && vc) ? col_get<FULL>(a.x + base + (size_t)pos * C, C, c)
-                                                 : make_double2(0.0, 0.0);
+      for (int m = 0; m < R; ++m)
+        v[m] = m < H ? *reinterpret_cast<const double2*>(st_in + (t + m * T) * W + 2 * g) : make_double2(0.0, 0.0);
+      __syncthreads();
+      const int nxt = tile + gridDim.x;
+      if (nxt < ntiles) {
+        const int on = nxt / ncb;
+        stage_cols<W>(st_in, a.x + (size_t)on * n * C + (size_t)(nxt - on * ncb) * W, n, C);
+      }
+      cp_async_commit();
+    } else {
+#pragma unroll
+      for (int m = 0; m < R; ++m) {
+        const int pos = t + m * T;
+        v[m] = (m < H && pos < n && vc) ? col_get<false>(a.x + base + (size_t)pos * C, C, c)
+                                        : make_double2(0.0, 0.0);
+      }
     }
     fft_lane<L, R, G, false>(v, S.ex, t, g, S.tw);
 #pragma unroll
-    for (int m = 0; m < R; ++m) v[m] = cmul(v[m], S.sym[t + m * T]);
+    for (int m = 0; m < R; ++m) v[m] = cmul(v[m], __ldg(&a.sym[t + m * T]));
     fft_lane<L, R, G, true>(v, S.ex, t, g, S.tw);
 
     if constexpr (MODE == 0) {
 #pragma unroll
       for (int m = 0; m < H; ++m) {
         const int pos = t + m * T;
-        if (!FULL && (pos >= n || !vc)) continue;
+        if (!PF && (pos >= n || !vc)) continue;
         const size_t o2 = base + (size_t)pos * C;
         double2 acc = make_double2(0.0, 0.0);
-        if (a.acc) acc = col_get<FULL>(a.acc + o2, C, c);
-        col_put<FULL>(a.out + o2, C, c, make_double2(acc.x + a.scale * v[m].x, acc.y + a.scale * v[m].y));
+        if (a.acc) acc = col_get<PF>(a.acc + o2, C, c);
+        col_put<PF>(a.out + o2, C, c, make_double2(acc.x + a.scale * v[m].x, acc.y + a.scale * v[m].y));
       }
     } else {
       // S mid pass: u is a.acc, w -> a.w, vp -> a.out
       const double im2 = a.inv_m2[o], a1 = a.a1[o];
-      const bool vb = FULL || c + 1 < C;
+      const bool vb = PF || c + 1 < C;
 #pragma unroll
       for (int m = 0; m < R; ++m) {
         const int pos = t + m * T;
-        if (m < H && (FULL || (pos < n && vc))) {
+        if (m < H && (PF || (pos < n && vc))) {
           const size_t o2 = base + (size_t)pos * C;
-          const double2 u = col_get<FULL>(a.acc + o2, C, c);
-          const double2 pv = col_get<FULL>(a.x + o2, C, c);
+          const double2 u = col_get<PF>(a.acc + o2, C, c);
+          const double2 pv = col_get<PF>(a.x + o2, C, c);
           const double bx = u.x + a.scale * v[m].x;
           const double by = u.y + a.scale * v[m].y;
           const double wx = bx * im2, wy = vb ? by * im2 : 0.0;
           e += a1 * pv.x * pv.x + wx * bx;
           if (vb) e += a1 * pv.y * pv.y + wy * by;
-          col_put<FULL>(a.w + o2, C, c, make_double2(wx, wy));
+          col_put<PF>(a.w + o2, C, c, make_double2(wx, wy));
           v[m] = make_double2(wx, wy);
         } else {
           v[m] = make_double2(0.0, 0.0);
@@ -322,15 +387,15 @@ __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_col(ColArgs a
       }
       fft_lane<L, R, G, false>(v, S.ex, t, g, S.tw);
 #pragma unroll
-      for (int m = 0; m < R; ++m) v[m] = cmul(v[m], S.sym[t + m * T]);
+      for (int m = 0; m < R; ++m) v[m] = cmul(v[m], __ldg(&a.sym[t + m * T]));
       fft_lane<L, R, G, true>(v, S.ex, t, g, S.tw);
 #pragma unroll
       for (int m = 0; m < H; ++m) {
         const int pos = t + m * T;
-        if (!FULL && (pos >= n || !vc)) continue;
+        if (!PF && (pos >= n || !vc)) continue;
         const size_t o2 = base + (size_t)pos * C;
-        const double2 pv = col_get<FULL>(a.x + o2, C, c);
-        col_put<FULL>(a.out + o2, C, c, make_double2(a.scale * v[m].x + a1 * pv.x, a.scale * v[m].y + a1 * pv.y));
+        const double2 pv = col_get<PF>(a.x + o2, C, c);
+        col_put<PF>(a.out + o2, C, c, make_double2(a.scale * v[m].x + a1 * pv.x, a.scale * v[m].y + a1 * pv.y));
       }
     }
   }
@@ -348,34 +413,65 @@ __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_col(ColArgs a
 // axis (spatial T. Chan eigenvalues are real and even; |conj(l_t) - s| =
 // |l_t - s| for real s), so F^-1 D F == H^-1 D H axis by axis: all three
 // passes stay real (N doubles in, N doubles out), see DESIGN.md.
-template <int N, bool FULL>
+template <int N, bool PF>
+struct HPlan {
+  using C = Cfg<N>;
+  static constexpr int TILE = PF ? 2 * C::G * N : 0;
+  using P = Plan<N, C::DB, 0, TILE>;
+  static constexpr size_t SMEM = P::BYTES;
+  using PT = Plan<N, C::DB, N, TILE>;  // t filter: lambda_t table after the twiddles
+  static constexpr size_t SMEM_T = PT::BYTES;
+};
+
+template <int N, bool PF>
 __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
     k_hartley_row(const double* in, double* out, int F, const double2* tw, const double* rdot, RedSlot red) {
   using Cf = Cfg<N>;
   constexpr int R = Cf::R, T = Cf::T, G = Cf::G;
+  constexpr int TILE = HPlan<N, PF>::TILE;
   extern __shared__ double2 smem_raw[];
   __shared__ double scratch[32];
-  Smem<N> S(smem_raw, tw, nullptr);
+  Smem<N, Cf::DB> S(smem_raw, tw, 0);
+  double* st_in = S.stage;
   const int g = threadIdx.x / T, t = threadIdx.x % T;  // lane-major: coalesced rows
   const int ntiles = (F + 2 * G - 1) / (2 * G);
+  if constexpr (PF) {
+    if (blockIdx.x < ntiles) stage_rows(st_in, in + (size_t)blockIdx.x * TILE, TILE);
+    cp_async_commit();
+  }
+  __syncthreads();
   double acc = 0.0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int f = (tile * G + g) * 2;
-    const bool va = FULL || f < F, vb = FULL || f + 1 < F;
+    const bool va = PF || f < F, vb = PF || f + 1 < F;
     const size_t ia = (size_t)f * N, ib = ia + N;
-    double2 v[R], w[R];
+    double2 v[R];
+    if constexpr (PF) {
+      cp_async_wait<0>();
+      __syncthreads();
 #pragma unroll
-    for (int m = 0; m < R; ++m) {
-      const int pos = t + m * T;
-      v[m].x = va ? __ldg(&in[ia + pos]) : 0.0;
-      v[m].y = vb ? __ldg(&in[ib + pos]) : 0.0;
+      for (int m = 0; m < R; ++m) {
+        const int pos = t + m * T;
+        v[m] = make_double2(st_in[(2 * g) * N + pos], st_in[(2 * g + 1) * N + pos]);
+      }
+      __syncthreads();
+      const int nxt = tile + gridDim.x;
+      if (nxt < ntiles) stage_rows(st_in, in + (size_t)nxt * TILE, TILE);
+      cp_async_commit();
+    } else {
+#pragma unroll
+      for (int m = 0; m < R; ++m) {
+        const int pos = t + m * T;
+        v[m].x = va ? __ldg(&in[ia + pos]) : 0.0;
+        v[m].y = vb ? __ldg(&in[ib + pos]) : 0.0;
+      }
     }
     fft_lane<N, R, G, false, 1>(v, S.ex, t, g, S.tw);
-    mirror_lane<N, R, G, 1>(v, w, S.ex, t, g);
+    hartley_lane<N, R, G, 1>(v, S.ex, t, g);
 #pragma unroll
     for (int m = 0; m < R; ++m) {
       const int pos = t + m * T;
-      const double2 h = hartley_split(v[m], w[m]);
+      const double2 h = v[m];
       if (va) {
         out[ia + pos] = h.x;
         if (rdot) acc += __ldg(&rdot[ia + pos]) * h.x;
@@ -393,61 +489,105 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
   }
 }
 
-template <int N, bool FULL>
+template <int N, bool PF>
 __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
     k_hartley_col(double* data, int O, int C, const double2* tw) {
   using Cf = Cfg<N>;
   constexpr int R = Cf::R, T = Cf::T, G = Cf::G;
+  constexpr int W = 2 * G;
   extern __shared__ double2 smem_raw[];
-  Smem<N> S(smem_raw, tw, nullptr);
+  Smem<N, Cf::DB> S(smem_raw, tw, 0);
+  double* st_in = S.stage;
   const int g = threadIdx.x % G, t = threadIdx.x / G;
-  const int ncb = (C + 2 * G - 1) / (2 * G);
+  const int ncb = (C + W - 1) / W;
   const int ntiles = ncb * O;
+  if constexpr (PF) {
+    if (blockIdx.x < ntiles) {
+      const int o = blockIdx.x / ncb;
+      stage_cols<W>(st_in, data + (size_t)o * N * C + (size_t)(blockIdx.x - o * ncb) * W, N, C);
+    }
+    cp_async_commit();
+  }
+  __syncthreads();
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int o = tile / ncb;
     const long c = (long)((tile - o * ncb) * G + g) * 2;
-    const bool vc = FULL || c < C;
+    const bool vc = PF || c < C;
     double* base = data + (size_t)o * N * C + c;
-    double2 v[R], w[R];
+    double2 v[R];
+    if constexpr (PF) {
+      cp_async_wait<0>();
+      __syncthreads();
 #pragma unroll
-    for (int m = 0; m < R; ++m)
-      v[m] = vc ? col_get<FULL>(base + (size_t)(t + m * T) * C, C, c) : make_double2(0.0, 0.0);
+      for (int m = 0; m < R; ++m) v[m] = *reinterpret_cast<const double2*>(st_in + (t + m * T) * W + 2 * g);
+      __syncthreads();
+      const int nxt = tile + gridDim.x;
+      if (nxt < ntiles) {
+        const int on = nxt / ncb;
+        stage_cols<W>(st_in, data + (size_t)on * N * C + (size_t)(nxt - on * ncb) * W, N, C);
+      }
+      cp_async_commit();
+    } else {
+#pragma unroll
+      for (int m = 0; m < R; ++m)
+        v[m] = vc ? col_get<false>(base + (size_t)(t + m * T) * C, C, c) : make_double2(0.0, 0.0);
+    }
     fft_lane<N, R, G, false>(v, S.ex, t, g, S.tw);
-    mirror_lane<N, R, G>(v, w, S.ex, t, g);
+    hartley_lane<N, R, G>(v, S.ex, t, g);
 #pragma unroll
     for (int m = 0; m < R; ++m)
-      if (vc) col_put<FULL>(base + (size_t)(t + m * T) * C, C, c, hartley_split(v[m], w[m]));
+      if (vc) col_put<PF>(base + (size_t)(t + m * T) * C, C, c, v[m]);
   }
 }
 
 // t pass of the preconditioner: Hartley along t, divide by lambda_S (computed
 // in registers from the 1-D eigenvalues, circulant.cpp:28-41, 76-90) and by
 // N (circulant.cpp:62-64), Hartley along t again.
-template <int N, bool FULL>
+template <int N, bool PF>
 __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(double* data, PcTables pt) {
   using Cf = Cfg<N>;
   constexpr int R = Cf::R, T = Cf::T, G = Cf::G;
+  constexpr int W = 2 * G;
   extern __shared__ double2 smem_raw[];
-  Smem<N> S(smem_raw, pt.tw_t, pt.lam_t);  // the "symbol" slot holds lambda_t
+  Smem<N, Cf::DB> S(smem_raw, pt.tw_t, N);
+  load_table(S.tab, pt.lam_t, N);
+  const double2* lamt = S.tab;
+  double* st_in = S.stage;
   const int g = threadIdx.x % G, t = threadIdx.x / G;
   const int C = pt.n1 * pt.n2;
-  const int ntiles = (C + 2 * G - 1) / (2 * G);
+  const int ntiles = (C + W - 1) / W;
+  if constexpr (PF) {
+    if (blockIdx.x < ntiles) stage_cols<W>(st_in, data + (size_t)blockIdx.x * W, N, C);
+    cp_async_commit();
+  }
+  __syncthreads();
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const long c = (long)(tile * G + g) * 2;
-    const bool vc = FULL || c < C;
-    double2 v[R], w[R];
+    const bool vc = PF || c < C;
+    double2 v[R];
+    if constexpr (PF) {
+      cp_async_wait<0>();
+      __syncthreads();
 #pragma unroll
-    for (int m = 0; m < R; ++m)
-      v[m] = vc ? col_get<FULL>(data + (size_t)(t + m * T) * C + c, C, c) : make_double2(0.0, 0.0);
+      for (int m = 0; m < R; ++m) v[m] = *reinterpret_cast<const double2*>(st_in + (t + m * T) * W + 2 * g);
+      __syncthreads();
+      const int nxt = tile + gridDim.x;
+      if (nxt < ntiles) stage_cols<W>(st_in, data + (size_t)nxt * W, N, C);
+      cp_async_commit();
+    } else {
+#pragma unroll
+      for (int m = 0; m < R; ++m)
+        v[m] = vc ? col_get<false>(data + (size_t)(t + m * T) * C + c, C, c) : make_double2(0.0, 0.0);
+    }
     fft_lane<N, R, G, false>(v, S.ex, t, g, S.tw);
-    mirror_lane<N, R, G>(v, w, S.ex, t, g);
+    hartley_lane<N, R, G>(v, S.ex, t, g);
     // spatial eigenvalue sums of the two packed columns
     double2 sa = make_double2(0.0, 0.0), sb = make_double2(0.0, 0.0);
     if (vc) {
       const int i = (int)(c / pt.n2), j = (int)(c - (long)i * pt.n2);
       const double2 l1 = __ldg(&pt.lam_1[i]), l2 = __ldg(&pt.lam_2[j]);
       sa = make_double2(l1.x + l2.x, l1.y + l2.y);
-      if (FULL || c + 1 < C) {
+      if (PF || c + 1 < C) {
         const int i2 = (int)((c + 1) / pt.n2), j2 = (int)(c + 1 - (long)i2 * pt.n2);
         const double2 m1 = __ldg(&pt.lam_1[i2]), m2 = __ldg(&pt.lam_2[j2]);
         sb = make_double2(m1.x + m2.x, m1.y + m2.y);
@@ -456,8 +596,8 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(doub
 #pragma unroll
     for (int m = 0; m < R; ++m) {
       const int k = t + m * T;
-      const double2 h = hartley_split(v[m], w[m]);
-      const double2 lt = S.sym[k];
+      const double2 h = v[m];
+      const double2 lt = lamt[k];
       const double bax = pt.psi * (lt.x - sa.x), bay = pt.psi * (lt.y - sa.y);
       const double bbx = pt.psi * (lt.x - sb.x), bby = pt.psi * (lt.y - sb.y);
       const double lsa = pt.base + (bax * bax + bay * bay) * pt.inv_m2;
@@ -467,10 +607,10 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(doub
       v[m] = make_double2(h.x * (lsb * inv), h.y * (lsa * inv));
     }
     fft_lane<N, R, G, false>(v, S.ex, t, g, S.tw);
-    mirror_lane<N, R, G>(v, w, S.ex, t, g);
+    hartley_lane<N, R, G>(v, S.ex, t, g);
 #pragma unroll
     for (int m = 0; m < R; ++m)
-      if (vc) col_put<FULL>(data + (size_t)(t + m * T) * C + c, C, c, hartley_split(v[m], w[m]));
+      if (vc) col_put<PF>(data + (size_t)(t + m * T) * C + c, C, c, v[m]);
   }
 }
 
