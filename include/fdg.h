@@ -180,9 +180,11 @@ fdg_status fdg_admm_objective(fdg_admm adm, double* out);
 
 /* Bench/roofline hook: average CUDA-event time (ms) of each kernel of one
  * PCG iteration over `reps` back-to-back launches, and its algorithmic HBM
- * bytes.  9 entries: K1 row(B), K2 x1 col(S mid), K3 row(B^T + r update),
- * P1 x2 Hartley, P2 x1 Hartley, P3 t filter, P4 x1 Hartley, P5 x2 Hartley
- * (+ r.z), K9 x/p update.  Clobbers the PCG scratch vectors. */
+ * bytes.  9 entries: K1 row (direction update p = z + b p fused with
+ * the B row pass), K2 x1 col (S mid), K3 row (B^T + r update), P1 x2
+ * Hartley, P2 x1 Hartley, P3 t filter, P4 x1 Hartley, P5 x2 Hartley (+ r.z),
+ * X x += a p.
+ * Clobbers the PCG scratch vectors. */
 fdg_status fdg_admm_profile_passes(fdg_admm adm, int reps, double* ms, double* bytes);
 
 /* --------------------------------------------------- synthetic inputs */

@@ -99,8 +99,8 @@ _sig("fdg_admm_objective", _st, _vp, _dp)
 _sig("fdg_admm_profile_passes", _st, _vp, C.c_int, _dp, _dp)
 _sig("fdg_admm_debug_get", _st, _vp, C.c_int, _dp)
 
-PASS_NAMES = ["K1_row_B", "K2_col_S_mid", "K3_row_BT_update", "P1_hartley_x2", "P2_hartley_x1",
-              "P3_t_filter", "P4_hartley_x1", "P5_hartley_x2_dot", "K9_cg_update"]
+PASS_NAMES = ["K1_row_p_update_B", "K2_col_S_mid", "K3_row_BT_update", "P1_hartley_x2",
+              "P2_hartley_x1", "P3_t_filter", "P4_hartley_x1", "P5_hartley_x2_dot", "X_axpy"]
 
 
 class FdgError(RuntimeError):

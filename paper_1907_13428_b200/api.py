@@ -352,7 +352,7 @@ class AdmmDriver:
         return float(out[0])
 
     def profile_passes(self, reps: int = 10) -> dict:
-        ms, by = np.zeros(9), np.zeros(9)
+        ms, by = np.zeros(len(N.PASS_NAMES)), np.zeros(len(N.PASS_NAMES))
         check(lib.fdg_admm_profile_passes(self.h, reps, _ptr(ms), _ptr(by)))
         return {n: dict(ms=float(m), bytes=float(b)) for n, m, b in zip(N.PASS_NAMES, ms, by)}
 

@@ -376,7 +376,7 @@ struct fdg_admm_s {
   // state (AdmmState admm.hpp:28-32) and work vectors
   DevBuf y, v, z_y, z_v, p, w_y, w_v, ybar, By;
   DevBuf rhs, r_cache, tmp;
-  DevBuf r, z, d, u, w, vp;  // PCG: residual, preconditioned residual, direction, scratch
+  DevBuf r, z, d, d2, u, w, vp;  // PCG: residual, preconditioned residual, directions (ping-pong), scratch
   Scalars sc;
   double inner_tol = 0.0;
   bool converged = false;
@@ -479,40 +479,92 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
     apply_S_dev(a, x, a->z.d());
     ck(fdg::launch_residual(st, lc, a->r.d(), rhs, a->z.d(), N, sc.slot(S_RR2)), "r = b - Ax");
   }
-  int cur = S_RZ0, nxt = S_RZ1;
-  pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(cur));
-  ck(fdg::launch_copy(st, lc, a->d.d(), a->z.d(), N), "p = z");
-  for (int it = 1; it <= max_inner; ++it) {
-    s_and_update(a, a->d.d(), sc.at(cur));
-    double pr[2];
-    sc.read(S_PQ, 2, pr);  // S_PQ, S_RR adjacent
-    const double pq = pr[0];
-    if (!std::isfinite(pq) || pq <= 0.0)
-      fail(FDG_ENUMERIC, "pcg: operator lost positive definiteness", FDG_NUM_PD_LOSS);
-    double rn = std::sqrt(pr[1]);
-    if (!std::isfinite(rn)) fail(FDG_ENUMERIC, "pcg: non-finite residual", FDG_NUM_NONFINITE_RESIDUAL);
-    bool x_done = false;
-    if (rn <= tol * nb) {
-      // confirm with the true residual (admm.cpp:152-158)
-      ck(fdg::launch_axpy_dev(st, lc, x, a->d.d(), N, sc.at(cur), sc.at(S_PQ)), "x += a p");
-      x_done = true;
-      apply_S_dev(a, x, a->z.d());
-      ck(fdg::launch_residual(st, lc, a->r.d(), rhs, a->z.d(), N, sc.slot(S_RR2)), "r = b - Ax");
-      double rr2;
-      sc.read(S_RR2, 1, &rr2);
-      rn = std::sqrt(rr2);
+  if (a->op->tf.kind != 2) {
+    // Fused schedule: the CG update x += a p; p = z + b p of
+    // iteration k-1 (p = z + b p) runs inside the B row pass of iteration k
+    // (K1F), with ping-pong direction buffers (neighbour time slices of the
+    // old direction stay readable while the new one is written); x += a p
+    // streams right after the S product, as in the reference loop.
+    int cur = S_RZ0, prv = S_RZ1;  // r.z of the current / previous residual
+    double* dcur = a->d.d();
+    double* dprv = a->d2.d();
+    bool first = true;
+    pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(cur));
+    fdg_op_s* op = a->op;
+    const TimeFactor& tf = op->tf;
+    for (int it = 1; it <= max_inner; ++it) {
+      ck(fdg::launch_row_fused(st, lc, a->z.d(), dprv, dcur, nullptr, a->u.d(), op->nt, op->n1, op->n2,
+                               op->row_axis(), op->scale2(), tf, op->psi, nullptr, nullptr, sc.at(cur), sc.at(prv),
+                               first, false),
+         "K1F row");
+      ck(fdg::launch_col_s_mid(st, lc, dcur, a->u.d(), a->w.d(), a->vp.d(), op->nt, op->n1, op->n2, op->ax1,
+                               op->scale1(), a->inv_m2.d(), a->a1.d(), sc.slot(S_PQ)),
+         "K2 col");
+      ck(fdg::launch_row_s_out(st, lc, a->w.d(), a->vp.d(), nullptr, a->r.d(), op->nt, op->n1, op->n2,
+                               op->row_axis(), op->scale2(), tf, op->psi, sc.at(cur), sc.at(S_PQ), sc.slot(S_RR)),
+         "K3 row");
+      ck(fdg::launch_axpy_dev(st, lc, x, dcur, N, sc.at(cur), sc.at(S_PQ)), "x += a p");
+      first = false;
+      double pr[2];
+      sc.read(S_PQ, 2, pr);  // S_PQ, S_RR adjacent
+      const double pq = pr[0];
+      if (!std::isfinite(pq) || pq <= 0.0)
+        fail(FDG_ENUMERIC, "pcg: operator lost positive definiteness", FDG_NUM_PD_LOSS);
+      double rn = std::sqrt(pr[1]);
+      if (!std::isfinite(rn)) fail(FDG_ENUMERIC, "pcg: non-finite residual", FDG_NUM_NONFINITE_RESIDUAL);
       if (rn <= tol * nb) {
-        res = {it, 1, rn / nb, 0.0};
-        finish();
-        return res;
+        // confirm with the true residual (admm.cpp:152-158)
+        apply_S_dev(a, x, a->z.d());
+        ck(fdg::launch_residual(st, lc, a->r.d(), rhs, a->z.d(), N, sc.slot(S_RR2)), "r = b - Ax");
+        double rr2;
+        sc.read(S_RR2, 1, &rr2);
+        rn = std::sqrt(rr2);
+        if (rn <= tol * nb) {
+          res = {it, 1, rn / nb, 0.0};
+          finish();
+          return res;
+        }
       }
+      pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(prv));  // r.z' -> prv slot
+      std::swap(cur, prv);
+      std::swap(dcur, dprv);
     }
-    pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(nxt));
-    // x += (rz/pq) p ; p = z + (rz'/rz) p  (admm.cpp:148-150, 161-163)
-    ck(fdg::launch_cg_update(st, lc, x, a->d.d(), a->z.d(), N, sc.at(cur), sc.at(S_PQ), sc.at(nxt), sc.at(cur),
-                             !x_done),
-       "cg update");
-    std::swap(cur, nxt);
+  } else {
+    int cur = S_RZ0, nxt = S_RZ1;
+    pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(cur));
+    ck(fdg::launch_copy(st, lc, a->d.d(), a->z.d(), N), "p = z");
+    for (int it = 1; it <= max_inner; ++it) {
+      s_and_update(a, a->d.d(), sc.at(cur));
+      double pr[2];
+      sc.read(S_PQ, 2, pr);  // S_PQ, S_RR adjacent
+      const double pq = pr[0];
+      if (!std::isfinite(pq) || pq <= 0.0)
+        fail(FDG_ENUMERIC, "pcg: operator lost positive definiteness", FDG_NUM_PD_LOSS);
+      double rn = std::sqrt(pr[1]);
+      if (!std::isfinite(rn)) fail(FDG_ENUMERIC, "pcg: non-finite residual", FDG_NUM_NONFINITE_RESIDUAL);
+      bool x_done = false;
+      if (rn <= tol * nb) {
+        // confirm with the true residual (admm.cpp:152-158)
+        ck(fdg::launch_axpy_dev(st, lc, x, a->d.d(), N, sc.at(cur), sc.at(S_PQ)), "x += a p");
+        x_done = true;
+        apply_S_dev(a, x, a->z.d());
+        ck(fdg::launch_residual(st, lc, a->r.d(), rhs, a->z.d(), N, sc.slot(S_RR2)), "r = b - Ax");
+        double rr2;
+        sc.read(S_RR2, 1, &rr2);
+        rn = std::sqrt(rr2);
+        if (rn <= tol * nb) {
+          res = {it, 1, rn / nb, 0.0};
+          finish();
+          return res;
+        }
+      }
+      pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(nxt));
+      // x += (rz/pq) p ; p = z + (rz'/rz) p  (admm.cpp:148-150, 161-163)
+      ck(fdg::launch_cg_update(st, lc, x, a->d.d(), a->z.d(), N, sc.at(cur), sc.at(S_PQ), sc.at(nxt), sc.at(cur),
+                               !x_done),
+         "cg update");
+      std::swap(cur, nxt);
+    }
   }
   // cap: true relative residual (admm.cpp:165-168)
   apply_S_dev(a, x, a->z.d());
@@ -942,7 +994,7 @@ fdg_status fdg_admm_create(fdg_op op, fdg_pc pc, const fdg_admm_desc* desc, cons
     upload(a->a1, a1, st);
     const size_t bytes = sizeof(double) * a->N;
     for (DevBuf* b : {&a->y, &a->v, &a->z_y, &a->z_v, &a->p, &a->w_y, &a->w_v, &a->ybar, &a->By, &a->rhs, &a->r_cache,
-                      &a->tmp, &a->r, &a->z, &a->d, &a->u, &a->w, &a->vp}) {
+                      &a->tmp, &a->r, &a->z, &a->d, &a->d2, &a->u, &a->w, &a->vp}) {
       b->alloc(bytes);
       ck(cudaMemsetAsync(b->p, 0, bytes, st), "memset");
     }
@@ -1095,7 +1147,7 @@ fdg_status fdg_admm_objective(fdg_admm a, double* out) {
 // hook).  Each pass is launched `reps` times back to back between two CUDA
 // events on the context stream.  Overwrites the PCG scratch vectors (run it
 // after the measurements that need them).  Order of ms[]: K1 row, K2 col,
-// K3 row, P1 x2, P2 x1, P3 t, P4 x1, P5 x2, K9 update.
+// K3 row, P1 x2, P2 x1, P3 t, P4 x1, P5 x2 (K1 = fused CG update + B row).
 fdg_status fdg_admm_profile_passes(fdg_admm a, int reps, double* ms, double* bytes) {
   return guard([&] {
     if (!a || reps < 1) fail(FDG_EINVAL, "fdg_admm_profile_passes: bad arguments");
@@ -1117,8 +1169,17 @@ fdg_status fdg_admm_profile_passes(fdg_admm a, int reps, double* ms, double* byt
       ck(cudaMemcpyAsync(sc.at(s), &one, sizeof(double), cudaMemcpyHostToDevice, st), "H2D");
     ck(cudaStreamSynchronize(st), "sync");
     std::vector<std::function<void()>> passes = {
-        [&] { ck(fdg::launch_row_apply(st, lc, a->d.d(), a->u.d(), op->nt, op->n1, op->n2, op->row_axis(), op->scale2(), stf,
-                                       op->psi, false), "K1"); },
+        [&] {
+          if (op->tf.kind != 2)
+            ck(fdg::launch_row_fused(st, lc, a->z.d(), a->d2.d(), a->d.d(), nullptr, a->u.d(), op->nt, op->n1,
+                                     op->n2, op->row_axis(), op->scale2(), stf, op->psi, nullptr, nullptr,
+                                     sc.at(S_RZ0), sc.at(S_RZ1), false, false),
+               "K1F");
+          else
+            ck(fdg::launch_row_apply(st, lc, a->d.d(), a->u.d(), op->nt, op->n1, op->n2, op->row_axis(),
+                                     op->scale2(), stf, op->psi, false),
+               "K1");
+        },
         [&] { ck(fdg::launch_col_s_mid(st, lc, a->d.d(), a->u.d(), a->w.d(), a->vp.d(), op->nt, op->n1, op->n2,
                                        op->ax1, op->scale1(), a->inv_m2.d(), a->a1.d(), sc.slot(S_DOT)), "K2"); },
         [&] { ck(fdg::launch_row_s_out(st, lc, a->w.d(), a->vp.d(), nullptr, a->r.d(), op->nt, op->n1, op->n2,
@@ -1131,12 +1192,13 @@ fdg_status fdg_admm_profile_passes(fdg_admm a, int reps, double* ms, double* byt
         [&] { ck(fdg::launch_hartley_col(st, lc, a->u.d(), pc->nt, pc->n1, pc->n2, pc->tab.tw_1), "P4"); },
         [&] { ck(fdg::launch_hartley_row(st, lc, a->u.d(), a->z.d(), F, pc->n2, pc->tab.tw_2, a->r.d(),
                                          sc.slot(S_DOT)), "P5"); },
-        [&] { ck(fdg::launch_cg_update(st, lc, a->tmp.d(), a->d.d(), a->z.d(), N, sc.at(S_RZ0), sc.at(S_PQ),
-                                       sc.at(S_RZ1), sc.at(S_RZ0), true), "K9"); },
+        [&] { ck(fdg::launch_axpy_dev(st, lc, a->tmp.d(), a->d.d(), N, sc.at(S_RZ0), sc.at(S_PQ)), "X"); },
     };
     // algorithmic HBM bytes per launch (each N-vector read or written once)
     const double nb = 8.0 * (double)N;
-    const double alg[9] = {2 * nb, 4 * nb, 4 * nb, 2 * nb, 2 * nb, 2 * nb, 2 * nb, 3 * nb, 5 * nb};
+    // K1F: reads z, d_old; writes d_new, u.  X: x += a p (3N).
+    const double k1 = op->tf.kind != 2 ? 4 * nb : 2 * nb;
+    const double alg[9] = {k1, 4 * nb, 4 * nb, 2 * nb, 2 * nb, 2 * nb, 2 * nb, 3 * nb, 3 * nb};
     for (size_t i = 0; i < passes.size(); ++i) {
       passes[i]();  // warm
       ck(cudaEventRecord(a->e0, st), "event");

@@ -76,6 +76,15 @@ cudaError_t launch_row_s_out(cudaStream_t st, LaunchCounter* lc, const double* w
                              double scale, const TimeFactor& tf, double psi, const double* alpha_num,
                              const double* alpha_den, RedSlot red);
 
+// Fused CG update + B row pass (K9 folded into K1): d_new = z + beta d_old
+// (beta = *b_num / *b_den; first: d_new = z), written to dnew and used as the
+// FFT input; u = row(d_new) like launch_row_apply; if upd_x: x += alpha d_old
+// (alpha = *a_num / *a_den).  Requires a bidiagonal or absent time factor.
+cudaError_t launch_row_fused(cudaStream_t st, LaunchCounter* lc, const double* z, const double* dold, double* dnew,
+                             double* xs, double* u, int nt, int n1, int n2, const AxisSym& s2, double scale,
+                             const TimeFactor& tf, double psi, const double* a_num, const double* a_den,
+                             const double* b_num, const double* b_den, bool first, bool upd_x);
+
 // Preconditioner passes (pow2 lengths).
 cudaError_t launch_hartley_row(cudaStream_t st, LaunchCounter* lc, const double* in, double* out, int F,
                                int n, const double2* tw, const double* rdot, RedSlot red);

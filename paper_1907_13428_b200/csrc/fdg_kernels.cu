@@ -321,6 +321,36 @@ cudaError_t launch_row_s_out(cudaStream_t st, LaunchCounter* lc, const double* w
   return dispatch_row<1>(st, s2.L, a);
 }
 
+cudaError_t launch_row_fused(cudaStream_t st, LaunchCounter* lc, const double* z, const double* dold, double* dnew,
+                             double* xs, double* u, int nt, int n1, int n2, const AxisSym& s2, double scale,
+                             const TimeFactor& tf, double psi, const double* a_num, const double* a_den,
+                             const double* b_num, const double* b_den, bool first, bool upd_x) {
+  RowArgs a{};
+  a.z = z;
+  a.dold = dold;
+  a.dnew = dnew;
+  a.xs = xs;
+  a.out = u;
+  a.nt = nt;
+  a.n1 = n1;
+  a.n = n2;
+  a.sym = s2.sym;
+  a.tw = s2.tw;
+  a.scale = scale;
+  a.tkind = tf.kind == 1 ? 1 : 0;
+  a.tc0 = 0.0;
+  a.tc1 = psi * tf.c1;
+  a.tdir = -1;
+  a.a_num = a_num;
+  a.a_den = a_den;
+  a.b_num = b_num;
+  a.b_den = b_den;
+  a.first = first ? 1 : 0;
+  a.upd_x = upd_x ? 1 : 0;
+  count(lc);
+  return dispatch_row<2>(st, s2.L, a);
+}
+
 cudaError_t launch_col_acc(cudaStream_t st, LaunchCounter* lc, const double* x, const double* acc, double* out,
                            int O, int n, int C, const AxisSym& s, double scale, bool adjoint) {
   ColArgs a{};

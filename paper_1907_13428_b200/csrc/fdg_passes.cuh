@@ -125,15 +125,26 @@ struct RowArgs {
   const double* a_num;
   const double* a_den;
   RedSlot red;
+  // MODE 2 (fused CG update + B row pass): d_new = z + beta d_old is the FFT
+  // input (written to dnew), x += alpha d_old (alpha = a_num/a_den).
+  const double* z;
+  const double* dold;
+  double* dnew;
+  double* xs;
+  const double* b_num;
+  const double* b_den;
+  int first;  // d_new = z (first Krylov iteration, no beta term, no x update)
+  int upd_x;  // apply x += alpha d_old
 };
 
 template <int L, int MODE, bool PF>
 struct RowPlan {
   using C = Cfg<L>;
   static constexpr int TILE = PF ? 2 * C::G * (L / 2) : 0;  // doubles per staged operand
-  static constexpr int NEPI = PF ? (MODE == 1 ? 3 : 1) : 0;
-  static constexpr bool DB = C::DB && !(PF && MODE == 1);
-  using P = Plan<L, DB, 0, TILE * (1 + NEPI)>;
+  static constexpr int NIN = MODE == 2 ? 2 : 1;  // staged input operands
+  static constexpr int NEPI = PF ? (MODE == 0 ? 1 : (MODE == 1 ? 3 : 2)) : 0;
+  static constexpr bool DB = C::DB && !(PF && MODE != 0);
+  using P = Plan<L, DB, 0, TILE * (NIN + NEPI)>;
   static constexpr size_t SMEM = P::BYTES;
 };
 
@@ -146,22 +157,35 @@ __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_row(RowArgs a
   extern __shared__ double2 smem_raw[];
   __shared__ double scratch[32];
   Smem<L, RP::DB> S(smem_raw, a.tw, 0);
-  double* st_in = S.stage;
-  double* st_nb = S.stage + TILE;
-  double* st_vp = S.stage + 2 * TILE;
-  double* st_r = S.stage + 3 * TILE;
+  double* st_in = S.stage;                    // FFT input (MODE 2: z)
+  double* st_in2 = S.stage + TILE;            // MODE 2: d_old
+  double* st_nb = S.stage + RP::NIN * TILE;   // neighbour row (MODE 2: z)
+  double* st_nb2 = st_nb + TILE;              // MODE 2: neighbour d_old
+  double* st_vp = S.stage + 2 * TILE;         // MODE 1
+  double* st_r = S.stage + 3 * TILE;          // MODE 1
   const int g = threadIdx.x / T, t = threadIdx.x % T;  // lane-major: coalesced rows
   const int F = a.nt * a.n1;
   const int ntiles = (F + 2 * G - 1) / (2 * G);
   const int n = a.n;
-  double alpha = 0.0;
+  double alpha = 0.0, beta = 0.0;
   if constexpr (MODE == 1) {
     if (a.r) alpha = *a.a_num / *a.a_den;
   }
+  if constexpr (MODE == 2) {
+    if (a.upd_x) alpha = *a.a_num / *a.a_den;
+    if (!a.first) beta = *a.b_num / *a.b_den;
+  }
+  const bool first = MODE == 2 && a.first;
+  // FFT input operand(s) of the pass
+  const double* in0 = MODE == 2 ? a.z : a.x;
+  const double* in1 = a.dold;
   const ptrdiff_t noff = (ptrdiff_t)a.tdir * a.n1 * n;
   double acc = 0.0;
   if constexpr (PF) {
-    if (blockIdx.x < ntiles) stage_rows(st_in, a.x + (size_t)blockIdx.x * 2 * G * n, TILE);
+    if (blockIdx.x < ntiles) {
+      stage_rows(st_in, in0 + (size_t)blockIdx.x * 2 * G * n, TILE);
+      if (MODE == 2 && !first) stage_rows(st_in2, in1 + (size_t)blockIdx.x * 2 * G * n, TILE);
+    }
     cp_async_commit();
   }
   __syncthreads();  // twiddle table
@@ -169,7 +193,7 @@ __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_row(RowArgs a
     const int f0 = tile * 2 * G;
     const int f = f0 + 2 * g;
     const bool va = PF || f < F, vb = PF || f + 1 < F;
-    const double* xa = a.x + (size_t)f * n;
+    const size_t ra = (size_t)f * n;  // row offset of the lane's first fibre
     double2 v[R];
     bool tile_nb = false;
     if constexpr (PF) {
@@ -178,20 +202,38 @@ __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_row(RowArgs a
 #pragma unroll
       for (int m = 0; m < R; ++m) {
         const int pos = t + m * T;
-        v[m] = m < H ? make_double2(st_in[(2 * g) * n + pos], st_in[(2 * g + 1) * n + pos])
-                     : make_double2(0.0, 0.0);
+        if (m < H) {
+          double2 z = make_double2(st_in[(2 * g) * n + pos], st_in[(2 * g + 1) * n + pos]);
+          if constexpr (MODE == 2) {
+            if (!first) {
+              z.x += beta * st_in2[(2 * g) * n + pos];
+              z.y += beta * st_in2[(2 * g + 1) * n + pos];
+            }
+            a.dnew[ra + pos] = z.x;
+            a.dnew[ra + n + pos] = z.y;
+          }
+          v[m] = z;
+        } else {
+          v[m] = make_double2(0.0, 0.0);
+        }
       }
       __syncthreads();  // st_in and the epilogue staging are free
       const int k = f0 / a.n1;  // whole tile in one slice
       tile_nb = a.tkind == 1 && (a.tdir < 0 ? k >= 1 : k + 1 < a.nt);
-      if (tile_nb) stage_rows(st_nb, a.x + (size_t)f0 * n + noff, TILE);
+      if (tile_nb) {
+        stage_rows(st_nb, in0 + (size_t)f0 * n + noff, TILE);
+        if (MODE == 2 && !first) stage_rows(st_nb2, in1 + (size_t)f0 * n + noff, TILE);
+      }
       if constexpr (MODE == 1) {
         stage_rows(st_vp, a.vp + (size_t)f0 * n, TILE);
         if (a.r) stage_rows(st_r, a.r + (size_t)f0 * n, TILE);
       }
       cp_async_commit();  // group E: this tile's epilogue operands
       const int nxt = tile + gridDim.x;
-      if (nxt < ntiles) stage_rows(st_in, a.x + (size_t)nxt * 2 * G * n, TILE);
+      if (nxt < ntiles) {
+        stage_rows(st_in, in0 + (size_t)nxt * 2 * G * n, TILE);
+        if (MODE == 2 && !first) stage_rows(st_in2, in1 + (size_t)nxt * 2 * G * n, TILE);
+      }
       cp_async_commit();  // group I: next tile's input
     } else {
 #pragma unroll
@@ -199,8 +241,16 @@ __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_row(RowArgs a
         const int pos = t + m * T;
         double2 z = make_double2(0.0, 0.0);
         if (m < H && pos < n) {
-          if (va) z.x = __ldg(xa + pos);
-          if (vb) z.y = __ldg(xa + n + pos);
+          if (va) z.x = __ldg(in0 + ra + pos);
+          if (vb) z.y = __ldg(in0 + ra + n + pos);
+          if constexpr (MODE == 2) {
+            if (!first) {
+              if (va) z.x += beta * __ldg(in1 + ra + pos);
+              if (vb) z.y += beta * __ldg(in1 + ra + n + pos);
+            }
+            if (va) a.dnew[ra + pos] = z.x;
+            if (vb) a.dnew[ra + n + pos] = z.y;
+          }
         }
         v[m] = z;
       }
@@ -225,15 +275,24 @@ __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_row(RowArgs a
       for (int h = 0; h < 2; ++h) {
         if (!PF && !(h ? vb : va)) continue;
         const int sl = (2 * g + h) * n + pos;  // staged element
+        const size_t o = ra + h * n + pos;
         double val = a.scale * (h ? v[m].y : v[m].x);
         if constexpr (PF) {
-          if (tile_nb) val += a.tc1 * st_nb[sl];
+          if (tile_nb) {
+            double nbv = st_nb[sl];
+            if (MODE == 2 && !first) nbv += beta * st_nb2[sl];
+            val += a.tc1 * nbv;
+          }
         } else {
-          if (h ? nbb : nba) val += a.tc1 * __ldg(xa + h * n + pos + noff);
+          if (h ? nbb : nba) {
+            double nbv = __ldg(in0 + o + noff);
+            if (MODE == 2 && !first) nbv += beta * __ldg(in1 + o + noff);
+            val += a.tc1 * nbv;
+          }
         }
-        const size_t o = (size_t)(f + h) * n + pos;
-        if constexpr (MODE == 0) {
+        if constexpr (MODE == 0 || MODE == 2) {
           a.out[o] = val;
+          if (MODE == 2 && a.upd_x) a.xs[o] += alpha * __ldg(in1 + o);  // x += alpha d_old
         } else {
           const double q = (PF ? st_vp[sl] : __ldg(&a.vp[o])) + val;
           if (a.q_out) a.q_out[o] = q;
