@@ -348,16 +348,17 @@ namespace {
 
 // z = S~^{-1} r via Hartley passes x2, x1, t(+divide), x1, x2.
 // h may alias z (not r).  rdot != null: reduce r.z into red.
-void pc_apply_dev(fdg_pc_s* pc, const double* r, double* z, double* h, const double* rdot, RedSlot red) {
+void pc_apply_dev(fdg_pc_s* pc, const double* r, double* z, double* h, const double* rdot, RedSlot red,
+                  const int* guard = nullptr) {
   cudaStream_t st = pc->ctx->stream;
   LaunchCounter* lc = &pc->ctx->lc;
   const int F = pc->nt * pc->n1;
   RedSlot none{};
-  ck(fdg::launch_hartley_row(st, lc, r, h, F, pc->n2, pc->tab.tw_2, nullptr, none), "pc x2 fwd");
-  ck(fdg::launch_hartley_col(st, lc, h, pc->nt, pc->n1, pc->n2, pc->tab.tw_1), "pc x1 fwd");
-  ck(fdg::launch_t_filter(st, lc, h, pc->tab), "pc t filter");
-  ck(fdg::launch_hartley_col(st, lc, h, pc->nt, pc->n1, pc->n2, pc->tab.tw_1), "pc x1 inv");
-  ck(fdg::launch_hartley_row(st, lc, h, z, F, pc->n2, pc->tab.tw_2, rdot, red), "pc x2 inv");
+  ck(fdg::launch_hartley_row(st, lc, r, h, F, pc->n2, pc->tab.tw_2, nullptr, none, guard), "pc x2 fwd");
+  ck(fdg::launch_hartley_col(st, lc, h, pc->nt, pc->n1, pc->n2, pc->tab.tw_1, guard), "pc x1 fwd");
+  ck(fdg::launch_t_filter(st, lc, h, pc->tab, guard), "pc t filter");
+  ck(fdg::launch_hartley_col(st, lc, h, pc->nt, pc->n1, pc->n2, pc->tab.tw_1, guard), "pc x1 inv");
+  ck(fdg::launch_hartley_row(st, lc, h, z, F, pc->n2, pc->tab.tw_2, rdot, red, guard), "pc x2 inv");
 }
 
 }  // namespace
@@ -383,6 +384,11 @@ struct fdg_admm_s {
   int stagnations = 0;
   int iteration = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
+  // speculative PCG: device pause flag, per-parity (pq, |r|^2) status, its
+  // pinned host mirror and completion events
+  DevBuf ctl, dstat;
+  double* hstat = nullptr;
+  cudaEvent_t ev_stat[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -485,50 +491,78 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
     // (K1F), with ping-pong direction buffers (neighbour time slices of the
     // old direction stay readable while the new one is written); x += a p
     // streams right after the S product, as in the reference loop.
-    int cur = S_RZ0, prv = S_RZ1;  // r.z of the current / previous residual
-    double* dcur = a->d.d();
-    double* dprv = a->d2.d();
-    bool first = true;
-    pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(cur));
+    //
+    // Speculation: iteration it+1 is enqueued before the host reads iteration
+    // it's scalars.  k_pcg_control(it) raises a device pause flag when the
+    // host must act (breakdown, or |r| <= tol |b| -> true-residual
+    // confirmation); every guarded kernel behind it then exits immediately,
+    // the host drains the stream, runs the reference's confirmation and
+    // re-enqueues.  Iteration parity fixes the ping-pong buffers and slots.
     fdg_op_s* op = a->op;
     const TimeFactor& tf = op->tf;
-    for (int it = 1; it <= max_inner; ++it) {
-      ck(fdg::launch_row_fused(st, lc, a->z.d(), dprv, dcur, nullptr, a->u.d(), op->nt, op->n1, op->n2,
-                               op->row_axis(), op->scale2(), tf, op->psi, nullptr, nullptr, sc.at(cur), sc.at(prv),
-                               first, false),
+    int* pause = static_cast<int*>(a->ctl.p);
+    double* dstat = a->dstat.d();
+    ck(cudaMemsetAsync(pause, 0, sizeof(int), st), "clear pause");
+    auto slot_cur = [](int it) { return (it & 1) ? S_RZ0 : S_RZ1; };  // r.z used by iteration it
+    auto slot_prv = [](int it) { return (it & 1) ? S_RZ1 : S_RZ0; };
+    auto dir_cur = [&](int it) { return (it & 1) ? a->d.d() : a->d2.d(); };
+    auto dir_prv = [&](int it) { return (it & 1) ? a->d2.d() : a->d.d(); };
+    // iteration body: S d, r -= a S d, x += a d, control, z = M r (r.z -> next slot)
+    auto enqueue = [&](int it, bool guarded) {
+      const int* g = guarded ? pause : nullptr;
+      const int cur = slot_cur(it), prv = slot_prv(it);
+      ck(fdg::launch_row_fused(st, lc, a->z.d(), dir_prv(it), dir_cur(it), nullptr, a->u.d(), op->nt, op->n1,
+                               op->n2, op->row_axis(), op->scale2(), tf, op->psi, nullptr, nullptr, sc.at(cur),
+                               sc.at(prv), it == 1, false, g),
          "K1F row");
-      ck(fdg::launch_col_s_mid(st, lc, dcur, a->u.d(), a->w.d(), a->vp.d(), op->nt, op->n1, op->n2, op->ax1,
-                               op->scale1(), a->inv_m2.d(), a->a1.d(), sc.slot(S_PQ)),
+      ck(fdg::launch_col_s_mid(st, lc, dir_cur(it), a->u.d(), a->w.d(), a->vp.d(), op->nt, op->n1, op->n2, op->ax1,
+                               op->scale1(), a->inv_m2.d(), a->a1.d(), sc.slot(S_PQ), g),
          "K2 col");
       ck(fdg::launch_row_s_out(st, lc, a->w.d(), a->vp.d(), nullptr, a->r.d(), op->nt, op->n1, op->n2,
-                               op->row_axis(), op->scale2(), tf, op->psi, sc.at(cur), sc.at(S_PQ), sc.slot(S_RR)),
+                               op->row_axis(), op->scale2(), tf, op->psi, sc.at(cur), sc.at(S_PQ), sc.slot(S_RR), g),
          "K3 row");
-      ck(fdg::launch_axpy_dev(st, lc, x, dcur, N, sc.at(cur), sc.at(S_PQ)), "x += a p");
-      first = false;
-      double pr[2];
-      sc.read(S_PQ, 2, pr);  // S_PQ, S_RR adjacent
-      const double pq = pr[0];
-      if (!std::isfinite(pq) || pq <= 0.0)
-        fail(FDG_ENUMERIC, "pcg: operator lost positive definiteness", FDG_NUM_PD_LOSS);
-      double rn = std::sqrt(pr[1]);
-      if (!std::isfinite(rn)) fail(FDG_ENUMERIC, "pcg: non-finite residual", FDG_NUM_NONFINITE_RESIDUAL);
-      if (rn <= tol * nb) {
-        // confirm with the true residual (admm.cpp:152-158)
-        apply_S_dev(a, x, a->z.d());
-        ck(fdg::launch_residual(st, lc, a->r.d(), rhs, a->z.d(), N, sc.slot(S_RR2)), "r = b - Ax");
-        double rr2;
-        sc.read(S_RR2, 1, &rr2);
-        rn = std::sqrt(rr2);
+      ck(fdg::launch_axpy_dev(st, lc, x, dir_cur(it), N, sc.at(cur), sc.at(S_PQ), g), "x += a p");
+      double* out = dstat + 4 * (it & 1);
+      ck(fdg::launch_pcg_control(st, lc, sc.at(S_PQ), sc.at(S_RR), (tol * nb) * (tol * nb), out, pause, g),
+         "control");
+      ck(cudaMemcpyAsync(a->hstat + 4 * (it & 1), out, 3 * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaEventRecord(a->ev_stat[it & 1], st), "event");
+      pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(prv), pause);  // r.z' -> prv slot
+    };
+    pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(slot_cur(1)));
+    if (max_inner >= 1) enqueue(1, true);
+    for (int it = 1; it <= max_inner; ++it) {
+      if (it < max_inner) enqueue(it + 1, true);  // speculative
+      ck(cudaEventSynchronize(a->ev_stat[it & 1]), "status");
+      const double* hs = a->hstat + 4 * (it & 1);
+      const double pq = hs[0];
+      double rn = std::sqrt(hs[1]);
+      if (hs[2] != 0.0) {
+        // iteration it paused the stream: drain the skipped launches
+        ck(cudaStreamSynchronize(st), "drain");
+        ck(cudaMemsetAsync(pause, 0, sizeof(int), st), "clear pause");
+        if (!std::isfinite(pq) || pq <= 0.0)
+          fail(FDG_ENUMERIC, "pcg: operator lost positive definiteness", FDG_NUM_PD_LOSS);
+        if (!std::isfinite(rn)) fail(FDG_ENUMERIC, "pcg: non-finite residual", FDG_NUM_NONFINITE_RESIDUAL);
         if (rn <= tol * nb) {
-          res = {it, 1, rn / nb, 0.0};
-          finish();
-          return res;
+          // confirm with the true residual (admm.cpp:152-158)
+          apply_S_dev(a, x, a->z.d());
+          ck(fdg::launch_residual(st, lc, a->r.d(), rhs, a->z.d(), N, sc.slot(S_RR2)), "r = b - Ax");
+          double rr2;
+          sc.read(S_RR2, 1, &rr2);
+          rn = std::sqrt(rr2);
+          if (rn <= tol * nb) {
+            res = {it, 1, rn / nb, 0.0};
+            finish();
+            return res;
+          }
         }
+        // continue (from the replaced residual): the skipped tail of it, then it+1
+        pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(slot_prv(it)));
+        if (it < max_inner) enqueue(it + 1, true);
       }
-      pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(prv));  // r.z' -> prv slot
-      std::swap(cur, prv);
-      std::swap(dcur, dprv);
     }
+    ck(cudaStreamSynchronize(st), "drain");
   } else {
     int cur = S_RZ0, nxt = S_RZ1;
     pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(cur));
@@ -1002,6 +1036,12 @@ fdg_status fdg_admm_create(fdg_op op, fdg_pc pc, const fdg_admm_desc* desc, cons
     a->sc.init(ctx);
     a->inner_tol = d.inner_tol_factor * d.inner_tol_floor;  // admm.cpp:245
     for (cudaEvent_t* e : {&a->e0, &a->e1, &a->e2, &a->e3}) ck(cudaEventCreate(e), "event");
+    for (cudaEvent_t* e : {&a->ev_stat[0], &a->ev_stat[1]})
+      ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
+    a->ctl.alloc(sizeof(int) * 4);
+    ck(cudaMemsetAsync(a->ctl.p, 0, sizeof(int) * 4, st), "memset");
+    a->dstat.alloc(sizeof(double) * 8);
+    ck(cudaMallocHost(&a->hstat, sizeof(double) * 8), "pinned");
     ck(cudaStreamSynchronize(st), "sync");
     *out = a.release();
   });
@@ -1012,8 +1052,9 @@ fdg_status fdg_admm_destroy(fdg_admm a) {
     if (!a) return;
     a->op->ctx->set_device();
     cudaStreamSynchronize(a->op->ctx->stream);
-    for (cudaEvent_t e : {a->e0, a->e1, a->e2, a->e3})
+    for (cudaEvent_t e : {a->e0, a->e1, a->e2, a->e3, a->ev_stat[0], a->ev_stat[1]})
       if (e) cudaEventDestroy(e);
+    if (a->hstat) cudaFreeHost(a->hstat);
     delete a;
   });
 }

@@ -67,14 +67,15 @@ cudaError_t launch_col_acc(cudaStream_t st, LaunchCounter* lc, const double* x, 
 // vp = scale*L1 w + a1[k] p; reduces sum(a1 p^2 + w Bp) = p^T S p.
 cudaError_t launch_col_s_mid(cudaStream_t st, LaunchCounter* lc, const double* p, const double* u,
                              double* w, double* vp, int nt, int n1, int n2, const AxisSym& s1,
-                             double scale, const double* inv_m2, const double* a1, RedSlot red);
+                             double scale, const double* inv_m2, const double* a1, RedSlot red,
+                             const int* guard = nullptr);
 
 // Fused S pass 3 (x2 rows) + residual update: q = vp + time^T(w) + scale*L2 w;
 // if q_out: q_out = q; if r: r -= alpha q with alpha = *num / *den, reduce |r|^2.
 cudaError_t launch_row_s_out(cudaStream_t st, LaunchCounter* lc, const double* w, const double* vp,
                              double* q_out, double* r, int nt, int n1, int n2, const AxisSym& s2,
                              double scale, const TimeFactor& tf, double psi, const double* alpha_num,
-                             const double* alpha_den, RedSlot red);
+                             const double* alpha_den, RedSlot red, const int* guard = nullptr);
 
 // Fused CG update + B row pass (K9 folded into K1): d_new = z + beta d_old
 // (beta = *b_num / *b_den; first: d_new = z), written to dnew and used as the
@@ -83,14 +84,23 @@ cudaError_t launch_row_s_out(cudaStream_t st, LaunchCounter* lc, const double* w
 cudaError_t launch_row_fused(cudaStream_t st, LaunchCounter* lc, const double* z, const double* dold, double* dnew,
                              double* xs, double* u, int nt, int n1, int n2, const AxisSym& s2, double scale,
                              const TimeFactor& tf, double psi, const double* a_num, const double* a_den,
-                             const double* b_num, const double* b_den, bool first, bool upd_x);
+                             const double* b_num, const double* b_den, bool first, bool upd_x,
+                             const int* guard = nullptr);
 
 // Preconditioner passes (pow2 lengths).
 cudaError_t launch_hartley_row(cudaStream_t st, LaunchCounter* lc, const double* in, double* out, int F,
-                               int n, const double2* tw, const double* rdot, RedSlot red);
+                               int n, const double2* tw, const double* rdot, RedSlot red,
+                               const int* guard = nullptr);
 cudaError_t launch_hartley_col(cudaStream_t st, LaunchCounter* lc, double* data, int O, int n, int C,
-                               const double2* tw);
-cudaError_t launch_t_filter(cudaStream_t st, LaunchCounter* lc, double* data, const PcTables& pt);
+                               const double2* tw, const int* guard = nullptr);
+cudaError_t launch_t_filter(cudaStream_t st, LaunchCounter* lc, double* data, const PcTables& pt,
+                            const int* guard = nullptr);
+
+// PCG control of one speculative iteration (1 thread): out[0] = pq,
+// out[1] = |r|^2 (copied for the host); raises *pause when the host must act
+// (pq <= 0 / non-finite, non-finite residual, or |r| <= tol |b|).
+cudaError_t launch_pcg_control(cudaStream_t st, LaunchCounter* lc, const double* pq, const double* rr,
+                               double tol_nb2, double* out, int* pause, const int* guard);
 
 // ------------------------------------------------------------- elementwise
 cudaError_t launch_copy(cudaStream_t st, LaunchCounter* lc, double* dst, const double* src, size_t N);
@@ -104,7 +114,7 @@ cudaError_t launch_cg_update(cudaStream_t st, LaunchCounter* lc, double* x, doub
                              const double* b_den, bool update_x);
 // x += alpha p only
 cudaError_t launch_axpy_dev(cudaStream_t st, LaunchCounter* lc, double* x, const double* p, size_t N,
-                            const double* a_num, const double* a_den);
+                            const double* a_num, const double* a_den, const int* guard = nullptr);
 // r = b - q, reduce |r|^2
 cudaError_t launch_residual(cudaStream_t st, LaunchCounter* lc, double* r, const double* b,
                             const double* q, size_t N, RedSlot red);

@@ -59,7 +59,11 @@ __global__ void k_cg_update(double* x, double* p, const double* z, size_t N, con
     p[i] = z[i] + beta * pi;
   }
 }
-__global__ void k_axpy_dev(double* x, const double* p, size_t N, const double* an, const double* ad) {
+__global__ void k_axpy_dev(double* x, const double* p, size_t N, const double* an, const double* ad,
+                           const int* guard) {
+  pdl_trigger();
+  pdl_wait();
+  if (guard && *reinterpret_cast<const volatile int*>(guard)) return;
   const double alpha = *an / *ad;
   GRID_STRIDE(i, N) x[i] += alpha * p[i];
 }
@@ -208,6 +212,25 @@ static inline void count(LaunchCounter* lc, unsigned long long k = 1) {
   if (lc) lc->count += k;
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel may begin
+// while its predecessor drains; it synchronizes with griddepcontrol.wait
+// (fdg_passes.cuh pdl_wait) before touching the predecessor's outputs.
+template <typename... KArgs, typename... Args>
+static cudaError_t pdl_launch(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 static inline unsigned clamp_grid(long tiles, int cap) {
   return (unsigned)(tiles < cap ? (tiles < 1 ? 1 : tiles) : cap);
 }
@@ -220,8 +243,7 @@ static cudaError_t run_row_v(cudaStream_t st, const RowArgs& a) {
   cudaError_t e = prep<k_row<L, MODE, PF>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
   const long F = (long)a.nt * a.n1;
-  k_row<L, MODE, PF><<<clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st>>>(a);
-  return cudaGetLastError();
+  return pdl_launch(k_row<L, MODE, PF>, clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st, a);
 }
 
 template <int L, int MODE>
@@ -252,8 +274,7 @@ static cudaError_t run_col_v(cudaStream_t st, const ColArgs& a) {
   cudaError_t e = prep<k_col<L, MODE, PF>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
   const long tiles = (long)a.O * ((a.C + 2 * Cf::G - 1) / (2 * Cf::G));
-  k_col<L, MODE, PF><<<clamp_grid(tiles, cap), Cf::THREADS, SM, st>>>(a);
-  return cudaGetLastError();
+  return pdl_launch(k_col<L, MODE, PF>, clamp_grid(tiles, cap), Cf::THREADS, SM, st, a);
 }
 
 template <int L, int MODE>
@@ -298,8 +319,9 @@ cudaError_t launch_row_apply(cudaStream_t st, LaunchCounter* lc, const double* x
 cudaError_t launch_row_s_out(cudaStream_t st, LaunchCounter* lc, const double* w, const double* vp, double* q_out,
                              double* r, int nt, int n1, int n2, const AxisSym& s2, double scale,
                              const TimeFactor& tf, double psi, const double* alpha_num, const double* alpha_den,
-                             RedSlot red) {
+                             RedSlot red, const int* guard) {
   RowArgs a{};
+  a.guard = guard;
   a.x = w;
   a.vp = vp;
   a.q_out = q_out;
@@ -324,8 +346,10 @@ cudaError_t launch_row_s_out(cudaStream_t st, LaunchCounter* lc, const double* w
 cudaError_t launch_row_fused(cudaStream_t st, LaunchCounter* lc, const double* z, const double* dold, double* dnew,
                              double* xs, double* u, int nt, int n1, int n2, const AxisSym& s2, double scale,
                              const TimeFactor& tf, double psi, const double* a_num, const double* a_den,
-                             const double* b_num, const double* b_den, bool first, bool upd_x) {
+                             const double* b_num, const double* b_den, bool first, bool upd_x,
+                             const int* guard) {
   RowArgs a{};
+  a.guard = guard;
   a.z = z;
   a.dold = dold;
   a.dnew = dnew;
@@ -369,8 +393,9 @@ cudaError_t launch_col_acc(cudaStream_t st, LaunchCounter* lc, const double* x, 
 
 cudaError_t launch_col_s_mid(cudaStream_t st, LaunchCounter* lc, const double* p, const double* u, double* w,
                              double* vp, int nt, int n1, int n2, const AxisSym& s1, double scale,
-                             const double* inv_m2, const double* a1, RedSlot red) {
+                             const double* inv_m2, const double* a1, RedSlot red, const int* guard) {
   ColArgs a{};
+  a.guard = guard;
   a.x = p;
   a.acc = u;
   a.w = w;
@@ -390,75 +415,73 @@ cudaError_t launch_col_s_mid(cudaStream_t st, LaunchCounter* lc, const double* p
 
 template <int N, bool PF>
 static cudaError_t run_hrow_v(cudaStream_t st, const double* in, double* out, int F, const double2* tw,
-                              const double* rdot, RedSlot red) {
+                              const double* rdot, RedSlot red, const int* guard) {
   using Cf = Cfg<N>;
   constexpr size_t SM = HPlan<N, PF>::SMEM;
   int cap = 0;
   cudaError_t e = prep<k_hartley_row<N, PF>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
-  k_hartley_row<N, PF><<<clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st>>>(in, out, F, tw,
-                                                                                                      rdot, red);
-  return cudaGetLastError();
+  return pdl_launch(k_hartley_row<N, PF>, clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st,
+                    in, out, F, tw, rdot, red, guard);
 }
 
 template <int N>
 static cudaError_t run_hrow(cudaStream_t st, const double* in, double* out, int F, const double2* tw,
-                            const double* rdot, RedSlot red) {
+                            const double* rdot, RedSlot red, const int* guard) {
   if constexpr (Cfg<N>::PF_OK) {
-    if (F % (2 * Cfg<N>::G) == 0) return run_hrow_v<N, true>(st, in, out, F, tw, rdot, red);
+    if (F % (2 * Cfg<N>::G) == 0) return run_hrow_v<N, true>(st, in, out, F, tw, rdot, red, guard);
   }
-  return run_hrow_v<N, false>(st, in, out, F, tw, rdot, red);
+  return run_hrow_v<N, false>(st, in, out, F, tw, rdot, red, guard);
 }
 
 template <int N, bool PF>
-static cudaError_t run_hcol_v(cudaStream_t st, double* data, int O, int C, const double2* tw) {
+static cudaError_t run_hcol_v(cudaStream_t st, double* data, int O, int C, const double2* tw, const int* guard) {
   using Cf = Cfg<N>;
   constexpr size_t SM = HPlan<N, PF>::SMEM;
   int cap = 0;
   cudaError_t e = prep<k_hartley_col<N, PF>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
   const long tiles = (long)O * ((C + 2 * Cf::G - 1) / (2 * Cf::G));
-  k_hartley_col<N, PF><<<clamp_grid(tiles, cap), Cf::THREADS, SM, st>>>(data, O, C, tw);
-  return cudaGetLastError();
+  return pdl_launch(k_hartley_col<N, PF>, clamp_grid(tiles, cap), Cf::THREADS, SM, st, data, O, C, tw, guard);
 }
 
 template <int N>
-static cudaError_t run_hcol(cudaStream_t st, double* data, int O, int C, const double2* tw) {
+static cudaError_t run_hcol(cudaStream_t st, double* data, int O, int C, const double2* tw, const int* guard) {
   if constexpr (Cfg<N>::PF_OK) {
-    if (C % (2 * Cfg<N>::G) == 0) return run_hcol_v<N, true>(st, data, O, C, tw);
+    if (C % (2 * Cfg<N>::G) == 0) return run_hcol_v<N, true>(st, data, O, C, tw, guard);
   }
-  return run_hcol_v<N, false>(st, data, O, C, tw);
+  return run_hcol_v<N, false>(st, data, O, C, tw, guard);
 }
 
 template <int N, bool PF>
-static cudaError_t run_tf_v(cudaStream_t st, double* data, const PcTables& pt) {
+static cudaError_t run_tf_v(cudaStream_t st, double* data, const PcTables& pt, const int* guard) {
   using Cf = Cfg<N>;
   constexpr size_t SM = HPlan<N, PF>::SMEM_T;
   int cap = 0;
   cudaError_t e = prep<k_t_filter<N, PF>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
   const long C = (long)pt.n1 * pt.n2;
-  k_t_filter<N, PF><<<clamp_grid((C + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st>>>(data, pt);
-  return cudaGetLastError();
+  return pdl_launch(k_t_filter<N, PF>, clamp_grid((C + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st, data,
+                    pt, guard);
 }
 
 template <int N>
-static cudaError_t run_tf(cudaStream_t st, double* data, const PcTables& pt) {
+static cudaError_t run_tf(cudaStream_t st, double* data, const PcTables& pt, const int* guard) {
   const long C = (long)pt.n1 * pt.n2;
   if constexpr (Cfg<N>::PF_OK) {
-    if (C % (2 * Cfg<N>::G) == 0) return run_tf_v<N, true>(st, data, pt);
+    if (C % (2 * Cfg<N>::G) == 0) return run_tf_v<N, true>(st, data, pt, guard);
   }
-  return run_tf_v<N, false>(st, data, pt);
+  return run_tf_v<N, false>(st, data, pt, guard);
 }
 
 #define FDG_POW2_CASES1(X) X(1) FDG_POW2_CASES(X)
 
 cudaError_t launch_hartley_row(cudaStream_t st, LaunchCounter* lc, const double* in, double* out, int F, int n,
-                               const double2* tw, const double* rdot, RedSlot red) {
+                               const double2* tw, const double* rdot, RedSlot red, const int* guard) {
   count(lc);
   switch (n) {
 #define X(NN) \
-  case NN: return run_hrow<NN>(st, in, out, F, tw, rdot, red);
+  case NN: return run_hrow<NN>(st, in, out, F, tw, rdot, red, guard);
     FDG_POW2_CASES1(X)
 #undef X
     default: return cudaErrorInvalidValue;
@@ -466,26 +489,53 @@ cudaError_t launch_hartley_row(cudaStream_t st, LaunchCounter* lc, const double*
 }
 
 cudaError_t launch_hartley_col(cudaStream_t st, LaunchCounter* lc, double* data, int O, int n, int C,
-                               const double2* tw) {
+                               const double2* tw, const int* guard) {
   count(lc);
   switch (n) {
 #define X(NN) \
-  case NN: return run_hcol<NN>(st, data, O, C, tw);
+  case NN: return run_hcol<NN>(st, data, O, C, tw, guard);
     FDG_POW2_CASES1(X)
 #undef X
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_t_filter(cudaStream_t st, LaunchCounter* lc, double* data, const PcTables& pt) {
+cudaError_t launch_t_filter(cudaStream_t st, LaunchCounter* lc, double* data, const PcTables& pt, const int* guard) {
   count(lc);
   switch (pt.nt) {
 #define X(NN) \
-  case NN: return run_tf<NN>(st, data, pt);
+  case NN: return run_tf<NN>(st, data, pt, guard);
     FDG_POW2_CASES1(X)
 #undef X
     default: return cudaErrorInvalidValue;
   }
+}
+
+// One thread: publish (pq, |r|^2) for the host and raise the pause flag when
+// the host has to intervene before the next (speculatively enqueued)
+// iteration may run: breakdown checks and the reference's true-residual
+// confirmation (admm.cpp:143-158).
+__global__ void k_pcg_control(const double* pq, const double* rr, double tol_nb2, double* out, int* pause,
+                              const int* guard) {
+  pdl_trigger();
+  pdl_wait();
+  if (guard && *reinterpret_cast<const volatile int*>(guard)) return;
+  const double p = *pq, r2 = *rr;
+  // slightly looser than the host's |r| <= tol |b| so that every host-side
+  // candidate has paused the stream; the host re-checks with the reference's
+  // exact comparison
+  const bool bad = !isfinite(p) || p <= 0.0 || !isfinite(r2);
+  const bool stop = bad || r2 <= tol_nb2 * (1.0 + 1e-12);
+  out[0] = p;
+  out[1] = r2;
+  out[2] = stop ? 1.0 : 0.0;
+  if (stop) *pause = 1;
+}
+
+cudaError_t launch_pcg_control(cudaStream_t st, LaunchCounter* lc, const double* pq, const double* rr,
+                               double tol_nb2, double* out, int* pause, const int* guard) {
+  count(lc);
+  return pdl_launch(k_pcg_control, 1, 1, 0, st, pq, rr, tol_nb2, out, pause, guard);
 }
 
 cudaError_t launch_copy(cudaStream_t st, LaunchCounter* lc, double* dst, const double* src, size_t N) {
@@ -512,10 +562,9 @@ cudaError_t launch_cg_update(cudaStream_t st, LaunchCounter* lc, double* x, doub
   return cudaGetLastError();
 }
 cudaError_t launch_axpy_dev(cudaStream_t st, LaunchCounter* lc, double* x, const double* p, size_t N,
-                            const double* a_num, const double* a_den) {
+                            const double* a_num, const double* a_den, const int* guard) {
   count(lc);
-  k_axpy_dev<<<ew_grid(N), EW_THREADS, 0, st>>>(x, p, N, a_num, a_den);
-  return cudaGetLastError();
+  return pdl_launch(k_axpy_dev, ew_grid(N), EW_THREADS, 0, st, x, p, N, a_num, a_den, guard);
 }
 cudaError_t launch_residual(cudaStream_t st, LaunchCounter* lc, double* r, const double* b, const double* q,
                             size_t N, RedSlot red) {

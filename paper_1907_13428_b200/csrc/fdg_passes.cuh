@@ -135,7 +135,23 @@ struct RowArgs {
   const double* b_den;
   int first;  // d_new = z (first Krylov iteration, no beta term, no x update)
   int upd_x;  // apply x += alpha d_old
+  const int* guard;  // speculative PCG iteration: skip the launch when *guard != 0
 };
+
+// Early exit of a speculatively enqueued PCG kernel (the host enqueues
+// iteration k+1 before it has read iteration k's scalars; the control kernel
+// of iteration k raises the pause flag when the host must intervene).
+__device__ __forceinline__ bool paused(const int* guard) {
+  return guard != nullptr && *reinterpret_cast<const volatile int*>(guard) != 0;
+}
+
+// Programmatic dependent launch: the pass kernels are launched with
+// programmatic stream serialization, so a kernel's CTAs may start (and stage
+// their twiddle tables) while the previous kernel drains its last tiles;
+// griddepcontrol.wait then blocks until the previous grid's memory is
+// visible.  Both are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
 template <int L, int MODE, bool PF>
 struct RowPlan {
@@ -157,6 +173,9 @@ __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_row(RowArgs a
   extern __shared__ double2 smem_raw[];
   __shared__ double scratch[32];
   Smem<L, RP::DB> S(smem_raw, a.tw, 0);
+  pdl_trigger();
+  pdl_wait();
+  if (paused(a.guard)) return;
   double* st_in = S.stage;                    // FFT input (MODE 2: z)
   double* st_in2 = S.stage + TILE;            // MODE 2: d_old
   double* st_nb = S.stage + RP::NIN * TILE;   // neighbour row (MODE 2: z)
@@ -332,6 +351,7 @@ struct ColArgs {
   const double* inv_m2;
   const double* a1;
   RedSlot red;
+  const int* guard;
 };
 
 template <bool FULL>
@@ -366,6 +386,9 @@ __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_col(ColArgs a
   extern __shared__ double2 smem_raw[];
   __shared__ double scratch[32];
   Smem<L, Cf::DB> S(smem_raw, a.tw, 0);
+  pdl_trigger();
+  pdl_wait();
+  if (paused(a.guard)) return;
   double* st_in = S.stage;
   const int g = threadIdx.x % G, t = threadIdx.x / G;
   const int n = a.n, C = a.C;
@@ -484,13 +507,17 @@ struct HPlan {
 
 template <int N, bool PF>
 __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
-    k_hartley_row(const double* in, double* out, int F, const double2* tw, const double* rdot, RedSlot red) {
+    k_hartley_row(const double* in, double* out, int F, const double2* tw, const double* rdot, RedSlot red,
+                  const int* guard) {
   using Cf = Cfg<N>;
   constexpr int R = Cf::R, T = Cf::T, G = Cf::G;
   constexpr int TILE = HPlan<N, PF>::TILE;
   extern __shared__ double2 smem_raw[];
   __shared__ double scratch[32];
   Smem<N, Cf::DB> S(smem_raw, tw, 0);
+  pdl_trigger();
+  pdl_wait();
+  if (paused(guard)) return;
   double* st_in = S.stage;
   const int g = threadIdx.x / T, t = threadIdx.x % T;  // lane-major: coalesced rows
   const int ntiles = (F + 2 * G - 1) / (2 * G);
@@ -550,12 +577,15 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
 
 template <int N, bool PF>
 __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
-    k_hartley_col(double* data, int O, int C, const double2* tw) {
+    k_hartley_col(double* data, int O, int C, const double2* tw, const int* guard) {
   using Cf = Cfg<N>;
   constexpr int R = Cf::R, T = Cf::T, G = Cf::G;
   constexpr int W = 2 * G;
   extern __shared__ double2 smem_raw[];
   Smem<N, Cf::DB> S(smem_raw, tw, 0);
+  pdl_trigger();
+  pdl_wait();
+  if (paused(guard)) return;
   double* st_in = S.stage;
   const int g = threadIdx.x % G, t = threadIdx.x / G;
   const int ncb = (C + W - 1) / W;
@@ -603,13 +633,16 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
 // in registers from the 1-D eigenvalues, circulant.cpp:28-41, 76-90) and by
 // N (circulant.cpp:62-64), Hartley along t again.
 template <int N, bool PF>
-__global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(double* data, PcTables pt) {
+__global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(double* data, PcTables pt, const int* guard) {
   using Cf = Cfg<N>;
   constexpr int R = Cf::R, T = Cf::T, G = Cf::G;
   constexpr int W = 2 * G;
   extern __shared__ double2 smem_raw[];
   Smem<N, Cf::DB> S(smem_raw, pt.tw_t, N);
   load_table(S.tab, pt.lam_t, N);
+  pdl_trigger();
+  pdl_wait();
+  if (paused(guard)) return;
   const double2* lamt = S.tab;
   double* st_in = S.stage;
   const int g = threadIdx.x % G, t = threadIdx.x / G;
