@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib", "libfdg.so")
 SOURCES = ["fdg_kernels.cu", "fdg_api.cu"]
-HEADERS = ["fdg_fft.cuh", "fdg_reduce.cuh", "fdg_internal.h"]
+HEADERS = ["fdg_fft.cuh", "fdg_passes.cuh", "fdg_conv.cuh", "fdg_reduce.cuh", "fdg_internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

@@ -281,6 +281,8 @@ struct fdg_op_s {
   double psi = 1.0;
   std::vector<double> tcol, trow, c1, r1, c2, r2;
   DevBuf sym1, tw1, sym2, tw2, symt, symt_adj, twt, sym2s;
+  DevBuf twh1, twh2, twht, tws1, tws2, twst;  // split passes: L/2-point twiddles, W_L^j (j < L/2)
+  DevBuf symr1, symr2, symrt, symr2s;          // real symbols of symmetric factors
   AxisSym ax1, ax2;
   AxisSym ax2s;  // x2 axis with the stencil diagonal folded in: sym2 - c0 (row passes)
   TimeFactor tf;
@@ -299,19 +301,44 @@ void upload(DevBuf& b, const std::vector<double>& h, cudaStream_t st) {
   ck(cudaStreamSynchronize(st), "sync");
 }
 
-void build_axis(fdg_op_s* op, AxisSym& ax, DevBuf& sym, DevBuf* sym_adj, DevBuf& tw, const std::vector<double>& col,
-                const std::vector<double>& row) {
+// Real parts of an interleaved complex table.
+std::vector<double> real_parts(const std::vector<double>& c) {
+  std::vector<double> r(c.size() / 2);
+  for (size_t i = 0; i < r.size(); ++i) r[i] = c[2 * i];
+  return r;
+}
+
+void build_axis(fdg_op_s* op, AxisSym& ax, DevBuf& sym, DevBuf* sym_adj, DevBuf& tw, DevBuf& twh, DevBuf& tws,
+                DevBuf& symr, const std::vector<double>& col, const std::vector<double>& row) {
   const int n = (int)col.size();
   const int L = std::max(2, pow2_ceil(2L * n - 1));
   if (L > 2048) fail(FDG_EUNSUPPORTED, "fdg: factor size " + std::to_string(n) + " exceeds the compiled kernel set (n <= 1024)");
   ax.n = n;
   ax.L = L;
-  upload(sym, embed_symbol_full(col, row, L), op->ctx->stream);
+  // A symmetric factor (row == col, e.g. the Riesz factors) has a real, even
+  // circulant spectrum: drop the rounding residue of the imaginary parts and
+  // keep a real copy for the split passes (real symbol multiply).
+  const bool symmetric = col == row;
+  std::vector<double> spec = embed_symbol_full(col, row, L);
+  if (symmetric) {
+    for (int f = 0; f < L; ++f) spec[2 * f + 1] = 0.0;
+    upload(symr, real_parts(spec), op->ctx->stream);
+    ax.sym_re = ax.sym_adj_re = symr.d();
+  }
+  upload(sym, spec, op->ctx->stream);
   upload(tw, stockham_twiddles(L), op->ctx->stream);
   ax.sym = sym.c();
   ax.tw = tw.c();
+  // split-spectrum passes (fdg_conv.cuh): M = L/2 point plan and W_L^j, j < M
+  const int M = std::max(1, L / 2);
+  upload(twh, stockham_twiddles(M), op->ctx->stream);
+  std::vector<double> twist = twiddles(L);
+  twist.resize(2 * (size_t)M);
+  upload(tws, twist, op->ctx->stream);
+  ax.twh = twh.c();
+  ax.twist = tws.c();
   ax.sym_adj = ax.sym;
-  if (sym_adj) {
+  if (sym_adj && !symmetric) {
     upload(*sym_adj, embed_symbol_full(row, col, L), op->ctx->stream);
     ax.sym_adj = sym_adj->c();
   }
@@ -775,8 +802,8 @@ fdg_status fdg_op_create(fdg_ctx ctx, int nt, int n1, int n2, const double* tcol
     // As in the reference, the adjoint transposes only the time factor; the
     // spatial passes use the forward symbols in both directions
     // (toeplitz.cpp:178-181, "Riesz factors are symmetric").
-    build_axis(op.get(), op->ax1, op->sym1, nullptr, op->tw1, op->c1, op->r1);
-    build_axis(op.get(), op->ax2, op->sym2, nullptr, op->tw2, op->c2, op->r2);
+    build_axis(op.get(), op->ax1, op->sym1, nullptr, op->tw1, op->twh1, op->tws1, op->symr1, op->c1, op->r1);
+    build_axis(op.get(), op->ax2, op->sym2, nullptr, op->tw2, op->twh2, op->tws2, op->symr2, op->c2, op->r2);
     bool bidiag = true;
     for (int k = 1; k < nt; ++k)
       if (op->trow[k] != 0.0) bidiag = false;
@@ -789,14 +816,20 @@ fdg_status fdg_op_create(fdg_ctx ctx, int nt, int n1, int n2, const double* tcol
       // psi c0 x_k == (-psi/L) IFFT(FFT(x) * (-c0 L)): fold the diagonal of the
       // time stencil into the x2 Toeplitz symbol (exact in real arithmetic).
       std::vector<double> s2 = embed_symbol_full(op->c2, op->r2, op->ax2.L);
+      if (op->ax2.sym_re)
+        for (int f = 0; f < op->ax2.L; ++f) s2[2 * f + 1] = 0.0;
       for (int f = 0; f < op->ax2.L; ++f) s2[2 * f] -= op->tf.c0;
       upload(op->sym2s, s2, ctx->stream);
       op->ax2s = op->ax2;
       op->ax2s.sym = op->sym2s.c();
       op->ax2s.sym_adj = op->sym2s.c();
+      if (op->ax2.sym_re) {
+        upload(op->symr2s, real_parts(s2), ctx->stream);
+        op->ax2s.sym_re = op->ax2s.sym_adj_re = op->symr2s.d();
+      }
     } else {
       op->tf.kind = 2;
-      build_axis(op.get(), op->tf.fft, op->symt, &op->symt_adj, op->twt, op->tcol, op->trow);
+      build_axis(op.get(), op->tf.fft, op->symt, &op->symt_adj, op->twt, op->twht, op->twst, op->symrt, op->tcol, op->trow);
       op->ax2s = op->ax2;
     }
     ctx->ensure_partials(fdg::max_partials_needed(nt, n1, n2));

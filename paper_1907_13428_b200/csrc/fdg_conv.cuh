@@ -1,0 +1,554 @@
+// fdg_conv.cuh — split-spectrum Toeplitz convolution passes (row and column).
+//
+// Same operator as the k_row / k_col passes of fdg_passes.cuh (reference:
+// ConstraintOperator::apply_mode, toeplitz.cpp:124-172): a Toeplitz matvec of
+// size n <= M = L/2 through its length-L circulant embedding.  Because the
+// input is zero beyond M and only the first M outputs are kept, the length-L
+// transform pair splits into two independent M-point pairs:
+//   X[2k]   = DFT_M(z)[k]                 X[2k+1] = DFT_M(z . W_L^j)[k]
+//   y[j]    = IDFT_M(s_e X_e)[j] + W_L^-j IDFT_M(s_o X_o)[j]      (j < M)
+// (s_e[k] = sym[2k], s_o[k] = sym[2k+1]).  A lane (two real fibres packed as
+// z = a + ib) is served by two sub-lanes of T = M/R threads that run the
+// even and the odd half at the same time, then one exchange adds the halves;
+// each sub-lane thread ends up owning R/2 output positions.
+//
+// For L = 512 (M = 256, R = 16) an M-point transform needs ONE shared-memory
+// exchange, so a convolution moves 5 x 256 values per sub-lane pair through
+// shared memory instead of 4 x 512 for the direct 512-point pair.
+//
+// Thread mapping (HOMO = 1): the first half of a CTA's threads are the even
+// sub-lanes of its G lanes, the second half the odd ones, so warps never
+// diverge on the odd half's twist multiplies W_L^{+-j}.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "fdg_fft.cuh"
+#include "fdg_passes.cuh"
+#include "fdg_reduce.cuh"
+
+namespace fdg {
+
+#ifndef FDG_C512_THREADS
+#define FDG_C512_THREADS 128
+#endif
+#ifndef FDG_C512_MINB_ROW
+#define FDG_C512_MINB_ROW 2
+#endif
+#ifndef FDG_C512_MINB_COL
+#define FDG_C512_MINB_COL 2
+#endif
+#ifndef FDG_C_HOMO
+#define FDG_C_HOMO 1
+#endif
+#ifndef FDG_C_EPI
+#define FDG_C_EPI 1
+#endif
+
+template <int L>
+struct CCfg {
+  static constexpr int M = L / 2;
+  static constexpr int R = fft_radix(M);
+  static constexpr int T = M / R;   // threads per sub-lane
+  static constexpr int LT = 2 * T;  // threads per lane
+  static constexpr int THREADS_ = L == 512 ? FDG_C512_THREADS : 256;
+  static constexpr int G = THREADS_ / LT < 1 ? 1 : THREADS_ / LT;  // lanes per CTA
+  static constexpr int G2 = 2 * G;                                 // sub-lanes per CTA
+  static constexpr int THREADS = G * LT;
+  static constexpr int MINB_ROW = L == 512 ? FDG_C512_MINB_ROW : 1;
+  static constexpr int MINB_COL = L == 512 ? FDG_C512_MINB_COL : 1;
+  static constexpr int HR = R / 2;               // output positions per thread
+  static constexpr size_t EXB = (size_t)M * G2;  // double2, one exchange buffer
+  static constexpr bool HOMO = FDG_C_HOMO != 0;
+  // sub-lane barriers assume T <= 32; the half-row swizzle a power-of-two G
+  static constexpr bool OK = T <= 32 && R >= 2 && (R & 1) == 0 && (G & (G - 1)) == 0;
+  // exchange | M-point twiddles | twist W_L^j (j < M) | symbol (L, real or
+  // complex) | staging
+  static constexpr size_t bytes(size_t stage_doubles, bool sr) {
+    return sizeof(double2) * (EXB + 2 * (size_t)M) + (sr ? sizeof(double) : sizeof(double2)) * (size_t)L +
+           sizeof(double) * stage_doubles;
+  }
+};
+
+// Symbol of the convolution in shared memory: real (symmetric Toeplitz
+// factor, SR) or complex.
+template <bool SR>
+struct SymTab {
+  const double* re;
+  const double2* c;
+  __device__ __forceinline__ double2 apply(double2 v, int k) const {
+    if constexpr (SR) {
+      return cscale(v, re[k]);
+    } else {
+      return cmul(v, c[k]);
+    }
+  }
+};
+
+template <int L, bool SR>
+struct CSmem {
+  Ex ex;
+  const double2* tw;
+  const double2* twist;
+  SymTab<SR> sym;
+  double* stage;
+  __device__ __forceinline__ CSmem(double2* base, const double2* gtw, const double2* gtwist, const double2* gsym,
+                                   const double* gsym_re) {
+    using C = CCfg<L>;
+    ex.buf0 = base;
+    ex.buf1 = base;
+    ex.k = 0;
+    double2* t = base + C::EXB;
+    load_table(t, gtw, C::M);
+    tw = t;
+    t += C::M;
+    load_table(t, gtwist, C::M);
+    twist = t;
+    t += C::M;
+    if constexpr (SR) {
+      double* d = reinterpret_cast<double*>(t);
+      for (int i = threadIdx.x; i < L; i += blockDim.x) d[i] = __ldg(&gsym_re[i]);
+      sym.re = d;
+      sym.c = nullptr;
+      stage = d + L;
+    } else {
+      load_table(t, gsym, L);
+      sym.c = t;
+      sym.re = nullptr;
+      stage = reinterpret_cast<double*>(t + L);
+    }
+  }
+};
+
+// Thread -> (lane g, half b, sub-lane thread t, sub-lane slot id gs, partner).
+template <int L, bool ROWS>
+struct CMap {
+  int g, b, t, gs, partner;
+  __device__ __forceinline__ CMap() {
+    using C = CCfg<L>;
+    const int tid = threadIdx.x;
+    if constexpr (C::HOMO) {
+      b = tid / (C::G * C::T);
+      const int r = tid - b * (C::G * C::T);
+      if constexpr (ROWS) {
+        g = r / C::T;
+        t = r - g * C::T;
+      } else {
+        t = r / C::G;
+        g = r - t * C::G;
+      }
+      gs = b * C::G + g;
+      partner = b ? gs - C::G : gs + C::G;
+    } else if constexpr (ROWS) {
+      g = tid / C::LT;
+      b = (tid / C::T) & 1;
+      t = tid % C::T;
+      gs = 2 * g + b;
+      partner = gs ^ 1;
+    } else {
+      gs = tid % C::G2;
+      t = tid / C::G2;
+      g = gs >> 1;
+      b = gs & 1;
+      partner = gs ^ 1;
+    }
+  }
+  // slot id holding the lane's half-b values
+  __device__ __forceinline__ int half_id(int h) const {
+    return CCfg<L>::HOMO ? h * CCfg<L>::G + g : 2 * g + h;
+  }
+};
+
+// Barrier over the two sub-lanes of every lane.
+template <int L, int LAYOUT>
+__device__ __forceinline__ void pair_sync() {
+  using C = CCfg<L>;
+  if constexpr (LAYOUT != 1 || C::HOMO || C::LT > 32) {
+    __syncthreads();
+  } else {
+    __syncwarp();
+  }
+}
+
+// Sub-lane b's half of the convolution, in place on v (input z[t + T m] for
+// every m; output that half's contribution at the same positions).
+template <int L, int LAYOUT, bool SR>
+__device__ __forceinline__ void conv_half(double2 (&v)[CCfg<L>::R], Ex& ex, int t, int gs, int b,
+                                          const double2* tw, const double2* twist, const SymTab<SR>& sym) {
+  using C = CCfg<L>;
+  constexpr int M = C::M, R = C::R, T = C::T, G2 = C::G2;
+#ifdef FDG_EXP_NOCONV
+  return;
+#endif
+  if (b) {
+#pragma unroll
+    for (int m = 0; m < R; ++m) v[m] = cmul(v[m], twist[t + T * m]);
+  }
+  fft_lane<M, R, G2, false, LAYOUT>(v, ex, t, gs, tw);
+#pragma unroll
+  for (int m = 0; m < R; ++m) v[m] = sym.apply(v[m], 2 * (t + T * m) + b);
+  fft_lane<M, R, G2, true, LAYOUT>(v, ex, t, gs, tw);
+  if (b) {
+#pragma unroll
+    for (int m = 0; m < R; ++m) v[m] = cmulc(v[m], twist[t + T * m]);
+  }
+}
+
+// Adds the two halves: half 0 owns positions t + T m for m < R/2, half 1
+// those for m >= R/2; y[i] is position t + T (i + b R/2).  Each store
+// instruction writes one half-row of both halves (conflict-free).  TRAIL:
+// barrier after the reads (when no other barrier precedes the next scatter).
+template <int L, int LAYOUT, bool TRAIL>
+__device__ __forceinline__ void conv_combine(const double2 (&v)[CCfg<L>::R], double2 (&y)[CCfg<L>::HR], Ex& ex,
+                                             const CMap<L, LAYOUT == 1>& mp) {
+  using C = CCfg<L>;
+  constexpr int M = C::M, T = C::T, G2 = C::G2, HR = C::HR;
+  const int t = mp.t, b = mp.b;
+#ifdef FDG_EXP_NOCOMB
+#pragma unroll
+  for (int i = 0; i < HR; ++i) y[i] = b ? v[i + HR] : v[i];
+  return;
+#endif
+  pair_sync<L, LAYOUT>();  // write-after-read: last inverse-FFT exchange
+  double2* sm = ex.next();
+#pragma unroll
+  for (int i = 0; i < HR; ++i) {
+    const double2 val = b ? v[i] : v[i + HR];
+    sm[slot<LAYOUT, M, G2>(t + T * (b ? i : i + HR), mp.gs)] = val;
+  }
+  pair_sync<L, LAYOUT>();
+#pragma unroll
+  for (int i = 0; i < HR; ++i) {
+    const double2 mine = b ? v[i + HR] : v[i];
+    y[i] = cadd(mine, sm[slot<LAYOUT, M, G2>(t + T * (i + b * HR), mp.partner)]);
+  }
+  if constexpr (TRAIL) pair_sync<L, LAYOUT>();
+}
+
+// =================================================================== rows
+template <int L, int MODE, bool PF, bool SR>
+struct RowCPlan {
+  using C = CCfg<L>;
+  static constexpr bool SEPI = PF && FDG_C_EPI != 0;      // staged epilogue operands
+  static constexpr int TILE = PF ? 2 * C::G * C::M : 0;  // doubles per staged operand
+  static constexpr int NIN = MODE == 2 ? 2 : 1;
+  static constexpr int NEPI = SEPI ? (MODE == 0 ? 1 : (MODE == 1 ? 3 : 2)) : 0;
+  static constexpr size_t SMEM = C::bytes((size_t)TILE * (NIN + NEPI), SR);
+};
+
+// Row pass along x2, modes as k_row (fdg_passes.cuh).  Lane-major exchange
+// layout (every sub-lane owns M contiguous slots).
+template <int L, int MODE, bool PF, bool SR>
+__global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(RowArgs a) {
+  using C = CCfg<L>;
+  using RP = RowCPlan<L, MODE, PF, SR>;
+  static_assert(C::OK, "split pass configuration");
+  constexpr int M = C::M, R = C::R, T = C::T, G = C::G, HR = C::HR;
+  constexpr int TILE = RP::TILE;
+  constexpr bool SEPI = RP::SEPI;
+  extern __shared__ double2 smem_raw[];
+  __shared__ double scratch[32];
+  CSmem<L, SR> S(smem_raw, a.twh, a.twist, a.sym, a.sym_re);
+  pdl_trigger();
+  pdl_wait();
+  if (paused(a.guard)) return;
+  double* st_in = S.stage;
+  double* st_in2 = S.stage + TILE;
+  double* st_nb = S.stage + RP::NIN * TILE;
+  double* st_nb2 = st_nb + TILE;
+  double* st_vp = S.stage + 2 * TILE;
+  double* st_r = S.stage + 3 * TILE;
+  const CMap<L, true> mp;
+  const int g = mp.g, b = mp.b, t = mp.t;
+  const int F = a.nt * a.n1;
+  const int ntiles = (F + 2 * G - 1) / (2 * G);
+  const int n = a.n;
+  double alpha = 0.0, beta = 0.0;
+  if constexpr (MODE == 1) {
+    if (a.r) alpha = *a.a_num / *a.a_den;
+  }
+  if constexpr (MODE == 2) {
+    if (a.upd_x) alpha = *a.a_num / *a.a_den;
+    if (!a.first) beta = *a.b_num / *a.b_den;
+  }
+  const bool first = MODE == 2 && a.first;
+  const double* in0 = MODE == 2 ? a.z : a.x;
+  const double* in1 = a.dold;
+  const ptrdiff_t noff = (ptrdiff_t)a.tdir * a.n1 * n;
+  double acc = 0.0;
+  if constexpr (PF) {
+    if (blockIdx.x < ntiles) {
+      stage_rows(st_in, in0 + (size_t)blockIdx.x * 2 * G * n, TILE);
+      if (MODE == 2 && !first) stage_rows(st_in2, in1 + (size_t)blockIdx.x * 2 * G * n, TILE);
+    }
+    cp_async_commit();
+  }
+  __syncthreads();  // tables
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int f0 = tile * 2 * G;
+    const int f = f0 + 2 * g;
+    const bool va = PF || f < F, vb = PF || f + 1 < F;
+    const size_t ra = (size_t)f * n;
+    double2 v[R];
+    bool tile_nb = false;
+    if constexpr (PF) {
+      cp_async_wait<0>();
+      __syncthreads();
+#pragma unroll
+      for (int m = 0; m < R; ++m) {
+        const int pos = t + m * T;
+        double2 z = make_double2(st_in[(2 * g) * M + pos], st_in[(2 * g + 1) * M + pos]);
+        if constexpr (MODE == 2) {
+          if (!first) {
+            z.x += beta * st_in2[(2 * g) * M + pos];
+            z.y += beta * st_in2[(2 * g + 1) * M + pos];
+          }
+          if ((m < HR) == (b == 0)) {
+            a.dnew[ra + pos] = z.x;
+            a.dnew[ra + n + pos] = z.y;
+          }
+        }
+        v[m] = z;
+      }
+      __syncthreads();  // st_in and the epilogue staging are free
+      const int k = f0 / a.n1;
+      tile_nb = a.tkind == 1 && (a.tdir < 0 ? k >= 1 : k + 1 < a.nt);
+      if constexpr (SEPI) {
+        if (tile_nb) {
+          stage_rows(st_nb, in0 + (size_t)f0 * n + noff, TILE);
+          if (MODE == 2 && !first) stage_rows(st_nb2, in1 + (size_t)f0 * n + noff, TILE);
+        }
+        if constexpr (MODE == 1) {
+          stage_rows(st_vp, a.vp + (size_t)f0 * n, TILE);
+          if (a.r) stage_rows(st_r, a.r + (size_t)f0 * n, TILE);
+        }
+      }
+      cp_async_commit();  // group E
+      const int nxt = tile + gridDim.x;
+      if (nxt < ntiles) {
+        stage_rows(st_in, in0 + (size_t)nxt * 2 * G * n, TILE);
+        if (MODE == 2 && !first) stage_rows(st_in2, in1 + (size_t)nxt * 2 * G * n, TILE);
+      }
+      cp_async_commit();  // group I
+    } else {
+#pragma unroll
+      for (int m = 0; m < R; ++m) {
+        const int pos = t + m * T;
+        double2 z = make_double2(0.0, 0.0);
+        if (pos < n) {
+          if (va) z.x = __ldg(in0 + ra + pos);
+          if (vb) z.y = __ldg(in0 + ra + n + pos);
+          if constexpr (MODE == 2) {
+            if (!first) {
+              if (va) z.x += beta * __ldg(in1 + ra + pos);
+              if (vb) z.y += beta * __ldg(in1 + ra + n + pos);
+            }
+            if ((m < HR) == (b == 0)) {
+              if (va) a.dnew[ra + pos] = z.x;
+              if (vb) a.dnew[ra + n + pos] = z.y;
+            }
+          }
+        }
+        v[m] = z;
+      }
+    }
+    conv_half<L, 1>(v, S.ex, t, mp.gs, b, S.tw, S.twist, S.sym);
+    double2 y[HR];
+    conv_combine<L, 1, !PF>(v, y, S.ex, mp);
+
+    if constexpr (SEPI) {
+      cp_async_wait<1>();
+      __syncthreads();
+    }
+    const int ka = f / a.n1, kb = (f + 1) / a.n1;
+    const bool nba = a.tkind == 1 && (a.tdir < 0 ? ka >= 1 : ka + 1 < a.nt);
+    const bool nbb = a.tkind == 1 && (a.tdir < 0 ? kb >= 1 : kb + 1 < a.nt);
+#pragma unroll
+    for (int i = 0; i < HR; ++i) {
+      const int pos = t + T * (i + b * HR);
+      if (!PF && pos >= n) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (!PF && !(h ? vb : va)) continue;
+        const int sl = (2 * g + h) * M + pos;
+        const size_t o = ra + h * n + pos;
+        double val = a.scale * (h ? y[i].y : y[i].x);
+        if constexpr (SEPI) {
+          if (tile_nb) {
+            double nbv = st_nb[sl];
+            if (MODE == 2 && !first) nbv += beta * st_nb2[sl];
+            val += a.tc1 * nbv;
+          }
+        } else {
+          if (h ? nbb : nba) {
+            double nbv = __ldg(in0 + o + noff);
+            if (MODE == 2 && !first) nbv += beta * __ldg(in1 + o + noff);
+            val += a.tc1 * nbv;
+          }
+        }
+        if constexpr (MODE == 0 || MODE == 2) {
+          a.out[o] = val;
+          if (MODE == 2 && a.upd_x) a.xs[o] += alpha * __ldg(in1 + o);
+        } else {
+          const double q = (SEPI ? st_vp[sl] : __ldg(&a.vp[o])) + val;
+          if (a.q_out) a.q_out[o] = q;
+          if (a.r) {
+            const double rn = (SEPI ? st_r[sl] : a.r[o]) - alpha * q;
+            a.r[o] = rn;
+            acc += rn * rn;
+          }
+        }
+      }
+    }
+  }
+  if constexpr (MODE == 1) {
+    if (a.r) {
+      double vv[1] = {acc};
+      block_reduce<RED_SUM, 1>(vv, scratch);
+      grid_finalize<RED_SUM, 1>(vv, a.red, scratch);
+    }
+  }
+}
+
+// ================================================================ columns
+template <int L, int MODE, bool PF, bool SR>
+struct ColCPlan {
+  using C = CCfg<L>;
+  static constexpr int TILE = PF ? 2 * C::G * C::M : 0;
+  // MODE 2: double-buffered input (p stays readable for both epilogues) + u
+  static constexpr int NST = MODE == 2 ? 3 : 1;
+  static constexpr size_t SMEM = C::bytes((size_t)TILE * NST, SR);
+};
+
+// Column pass, modes as k_col (fdg_passes.cuh).  Interleaved exchange layout
+// (rows of G2 sub-lanes; split-interleaved when HOMO), sub-lanes of lane g
+// serve columns (2g, 2g+1) of the tile.
+template <int L, int MODE, bool PF, bool SR>
+__global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(ColArgs a) {
+  using Cf = CCfg<L>;
+  static_assert(Cf::OK, "split pass configuration");
+  constexpr int M = Cf::M, R = Cf::R, T = Cf::T, G = Cf::G, G2 = Cf::G2, HR = Cf::HR;
+  constexpr int LY = Cf::HOMO ? 2 : 0;
+  constexpr int W = 2 * G;
+  extern __shared__ double2 smem_raw[];
+  __shared__ double scratch[32];
+  CSmem<L, SR> S(smem_raw, a.twh, a.twist, a.sym, a.sym_re);
+  pdl_trigger();
+  pdl_wait();
+  if (paused(a.guard)) return;
+  constexpr int TILE = ColCPlan<L, MODE, PF, SR>::TILE;
+  const CMap<L, false> mp;
+  const int g = mp.g, b = mp.b, t = mp.t;
+  const int n = a.n, C = a.C;
+  const int ncb = (C + W - 1) / W;
+  const int ntiles = ncb * a.O;
+  // staged column tile [pos][W] of `src` for tile index tl
+  auto stage_tile = [&](double* dst, const double* src, int tl) {
+    const int ot = tl / ncb;
+    stage_cols<W>(dst, src + (size_t)ot * n * C + (size_t)(tl - ot * ncb) * W, n, C);
+  };
+  double* st_u = S.stage + 2 * TILE;  // MODE 2
+  if constexpr (PF) {
+    if (blockIdx.x < ntiles) {
+      stage_tile(S.stage, a.x, blockIdx.x);
+      if constexpr (MODE == 2) stage_tile(st_u, a.acc, blockIdx.x);
+    }
+    cp_async_commit();
+  }
+  __syncthreads();  // tables
+  double e = 0.0;
+  int buf = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= (MODE == 2)) {
+    const int o = tile / ncb;
+    const long c = (long)((tile - o * ncb) * G + g) * 2;
+    const bool vc = PF || c < C;
+    const bool vb = PF || c + 1 < C;
+    const size_t base = (size_t)o * n * C + c;
+    const int nxt = tile + gridDim.x;
+    double* st_in = S.stage + buf * TILE;
+    double2 v[R];
+    if constexpr (PF) {
+      cp_async_wait<0>();
+      __syncthreads();
+#pragma unroll
+      for (int m = 0; m < R; ++m) v[m] = *reinterpret_cast<const double2*>(st_in + (t + m * T) * W + 2 * g);
+      if constexpr (MODE != 2) __syncthreads();  // single input buffer
+      if (nxt < ntiles) stage_tile(S.stage + (buf ^ (MODE == 2)) * TILE, a.x, nxt);
+      cp_async_commit();
+    } else {
+#pragma unroll
+      for (int m = 0; m < R; ++m) {
+        const int pos = t + m * T;
+        v[m] = (pos < n && vc) ? col_get<false>(a.x + base + (size_t)pos * C, C, c) : make_double2(0.0, 0.0);
+      }
+    }
+    conv_half<L, LY>(v, S.ex, t, mp.gs, b, S.tw, S.twist, S.sym);
+    double2 y[HR];
+    conv_combine<L, LY, !PF && MODE == 0>(v, y, S.ex, mp);
+
+    if constexpr (MODE == 0) {
+#pragma unroll
+      for (int i = 0; i < HR; ++i) {
+        const int pos = t + T * (i + b * HR);
+        if (!PF && (pos >= n || !vc)) continue;
+        const size_t o2 = base + (size_t)pos * C;
+        double2 acc = make_double2(0.0, 0.0);
+        if (a.acc) acc = col_get<PF>(a.acc + o2, C, c);
+        col_put<PF>(a.out + o2, C, c, make_double2(acc.x + a.scale * y[i].x, acc.y + a.scale * y[i].y));
+      }
+    } else {
+      // S mid pass: Bp = u + scale L1 p; w = Bp / m2[o] (-> a.w, and the
+      // input of the second convolution); vp = scale L1 w + a1 p (-> a.out)
+      const double im2 = a.inv_m2[o], a1 = a.a1[o];
+#pragma unroll
+      for (int i = 0; i < HR; ++i) {
+        const int pos = t + T * (i + b * HR);
+        if (PF || (pos < n && vc)) {
+          const size_t o2 = base + (size_t)pos * C;
+          const double2 u = PF ? *reinterpret_cast<const double2*>(st_u + pos * W + 2 * g) : col_get<PF>(a.acc + o2, C, c);
+          const double2 pv = PF ? *reinterpret_cast<const double2*>(st_in + pos * W + 2 * g) : col_get<PF>(a.x + o2, C, c);
+          const double bx = u.x + a.scale * y[i].x;
+          const double by = u.y + a.scale * y[i].y;
+          const double wx = bx * im2, wy = vb ? by * im2 : 0.0;
+          e += a1 * pv.x * pv.x + wx * bx;
+          if (vb) e += a1 * pv.y * pv.y + wy * by;
+          col_put<PF>(a.w + o2, C, c, make_double2(wx, wy));
+          y[i] = make_double2(wx, wy);
+        } else {
+          y[i] = make_double2(0.0, 0.0);
+        }
+      }
+      // both halves need all of w: each writes its positions into its own
+      // slot column, then reads the lane's full column pair
+      __syncthreads();  // write-after-read: combine (and every read of st_u)
+      if constexpr (PF) {
+        if (nxt < ntiles) stage_tile(st_u, a.acc, nxt);
+        cp_async_commit();
+      }
+      double2* sm = S.ex.next();
+#pragma unroll
+      for (int i = 0; i < HR; ++i) sm[slot<LY, M, G2>(t + T * (i + b * HR), mp.gs)] = y[i];
+      __syncthreads();
+      const int id0 = mp.half_id(0), id1 = mp.half_id(1);
+#pragma unroll
+      for (int m = 0; m < R; ++m) v[m] = sm[slot<LY, M, G2>(t + T * m, m < HR ? id0 : id1)];
+      conv_half<L, LY>(v, S.ex, t, mp.gs, b, S.tw, S.twist, S.sym);
+      conv_combine<L, LY, !PF>(v, y, S.ex, mp);
+#pragma unroll
+      for (int i = 0; i < HR; ++i) {
+        const int pos = t + T * (i + b * HR);
+        if (!PF && (pos >= n || !vc)) continue;
+        const size_t o2 = base + (size_t)pos * C;
+        const double2 pv = PF ? *reinterpret_cast<const double2*>(st_in + pos * W + 2 * g) : col_get<PF>(a.x + o2, C, c);
+        col_put<PF>(a.out + o2, C, c, make_double2(a.scale * y[i].x + a1 * pv.x, a.scale * y[i].y + a1 * pv.y));
+      }
+    }
+  }
+  if constexpr (MODE == 2) {
+    double vv[1] = {e};
+    block_reduce<RED_SUM, 1>(vv, scratch);
+    grid_finalize<RED_SUM, 1>(vv, a.red, scratch);
+  }
+}
+
+}  // namespace fdg

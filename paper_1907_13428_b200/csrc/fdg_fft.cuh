@@ -159,10 +159,23 @@ __device__ __forceinline__ int lidx(int pos, int g) {
   return g * N + (pos ^ (f & 7));
 }
 
-// LAYOUT 0: lane-interleaved rows of G (column passes); 1: lane-major.
+// Split-interleaved slot (fdg_conv.cuh column passes, warps holding only
+// even- or only odd-half sub-lanes): rows of G lanes whose two halves (G/2
+// sub-lanes each) are swapped on rows of odd popcount, so the 32/(G/2)
+// positions a half-row warp touches always fill complementary halves of the
+// 128-byte bank window (any power-of-two position pattern has half of its
+// positions at odd popcount).
+template <int G>
+__device__ __forceinline__ int hidx(int pos, int g) {
+  return pos * G + (g ^ ((__popc(pos) & 1) * (G / 2)));
+}
+
+// LAYOUT 0: lane-interleaved rows of G (column passes); 1: lane-major;
+// 2: split-interleaved (hidx).
 template <int LAYOUT, int N, int G>
 __device__ __forceinline__ int slot(int pos, int g) {
   if constexpr (LAYOUT == 0) return sidx<G>(pos, g);
+  else if constexpr (LAYOUT == 2) return hidx<G>(pos, g);
   else return lidx<N>(pos, g);
 }
 
@@ -189,7 +202,7 @@ struct Ex {
 // then run their FFTs independently instead of in CTA-wide lock step.
 template <int LAYOUT, int T>
 __device__ __forceinline__ void lane_sync(int g) {
-  if constexpr (LAYOUT == 0) {
+  if constexpr (LAYOUT == 0 || LAYOUT == 2) {
     __syncthreads();
   } else if constexpr (T <= 32) {
     __syncwarp();
@@ -200,7 +213,15 @@ __device__ __forceinline__ void lane_sync(int g) {
 
 // Registers per thread (= radix bound) used for a transform of length N;
 // shared by the kernels (Cfg) and the host twiddle-table builder.
-__host__ __device__ constexpr int fft_radix(int N) { return N <= 8 ? N : (N <= 512 ? 8 : 16); }
+#ifndef FDG_R256
+#define FDG_R256 16
+#endif
+#ifndef FDG_R512
+#define FDG_R512 8
+#endif
+__host__ __device__ constexpr int fft_radix(int N) {
+  return N <= 8 ? N : (N == 256 ? FDG_R256 : (N == 512 ? FDG_R512 : (N < 512 ? 8 : 16)));
+}
 
 // Compile-time radix plan: passes of radix min(R, N/Ns).
 template <int N, int R, int Ns>
@@ -246,15 +267,22 @@ struct Stockham {
             wt[r] = cmul(wt[lo], wt[r - lo]);
           }
         }
+#ifndef FDG_EXP_NOMATH
 #pragma unroll
         for (int r = 1; r < Rp; ++r) v[s + r * S] = INV ? cmulc(v[s + r * S], wt[r]) : cmul(v[s + r * S], wt[r]);
+#else
+        v[s + S] = cadd(v[s + S], wt[1]);
+#endif
       }
+#ifndef FDG_EXP_NOMATH
       Dft<Rp, INV>::run(v, s, S);
+#endif
     }
     if constexpr (!LAST) {
       if (ex.single()) lane_sync<LAYOUT, T>(g);  // write-after-read on the single buffer
       double2* sm = ex.next();
       // scatter: out[(b/Ns)*Ns*Rp + b%Ns + r*Ns] = v[s + r*S]
+#ifndef FDG_EXP_NOEX
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const int b = t + s * T;
@@ -262,9 +290,12 @@ struct Stockham {
 #pragma unroll
         for (int r = 0; r < Rp; ++r) sm[slot<LAYOUT, N, G>(base + r * Ns, g)] = v[s + r * S];
       }
+#endif
       lane_sync<LAYOUT, T>(g);
+#ifndef FDG_EXP_NOEX
 #pragma unroll
       for (int m = 0; m < R; ++m) v[m] = sm[slot<LAYOUT, N, G>(t + m * T, g)];
+#endif
       Stockham<N, R, G, INV, Ns * Rp, LAYOUT, NEXT_OFF>::run(v, ex, t, g, ptw);
     }
   }

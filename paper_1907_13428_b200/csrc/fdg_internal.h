@@ -20,6 +20,10 @@ struct AxisSym {
   const double2* sym = nullptr;      // forward factor symbol
   const double2* sym_adj = nullptr;  // transposed factor symbol (== sym if symmetric)
   const double2* tw = nullptr;       // W_L twiddles
+  const double2* twh = nullptr;      // per-pass twiddles of the L/2-point transform
+  const double2* twist = nullptr;    // W_L^j, j < L/2 (split passes, fdg_conv.cuh)
+  const double* sym_re = nullptr;      // real copy of sym when the factor is symmetric
+  const double* sym_adj_re = nullptr;  // real copy of sym_adj
 };
 
 // Time coupling.  kind 0: no time term; 1: lower-bidiagonal stencil

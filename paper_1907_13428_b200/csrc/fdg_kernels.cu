@@ -18,6 +18,7 @@
 #include "fdg_fft.cuh"
 #include "fdg_internal.h"
 #include "fdg_passes.cuh"
+#include "fdg_conv.cuh"
 #include "fdg_reduce.cuh"
 
 namespace fdg {
@@ -235,8 +236,51 @@ static inline unsigned clamp_grid(long tiles, int cap) {
   return (unsigned)(tiles < cap ? (tiles < 1 ? 1 : tiles) : cap);
 }
 
+#ifndef FDG_SPLIT_CONV
+#define FDG_SPLIT_CONV 1
+#endif
+// Embedding lengths served by the split-spectrum passes (fdg_conv.cuh).
+template <int L>
+struct UseSplit {
+  static constexpr bool value = FDG_SPLIT_CONV && L == 512;
+};
+
+template <int L, int MODE, bool PF, bool SR>
+static cudaError_t run_rowc_s(cudaStream_t st, const RowArgs& a) {
+  using Cf = CCfg<L>;
+  constexpr size_t SM = RowCPlan<L, MODE, PF, SR>::SMEM;
+  int cap = 0;
+  cudaError_t e = prep<k_rowc<L, MODE, PF, SR>>(SM, Cf::THREADS, cap);
+  if (e != cudaSuccess) return e;
+  const long F = (long)a.nt * a.n1;
+  return pdl_launch(k_rowc<L, MODE, PF, SR>, clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st,
+                    a);
+}
+template <int L, int MODE, bool PF>
+static cudaError_t run_rowc_v(cudaStream_t st, const RowArgs& a) {
+  return a.sym_re ? run_rowc_s<L, MODE, PF, true>(st, a) : run_rowc_s<L, MODE, PF, false>(st, a);
+}
+
+template <int L, int MODE, bool PF, bool SR>
+static cudaError_t run_colc_s(cudaStream_t st, const ColArgs& a) {
+  using Cf = CCfg<L>;
+  constexpr size_t SM = ColCPlan<L, MODE, PF, SR>::SMEM;
+  int cap = 0;
+  cudaError_t e = prep<k_colc<L, MODE, PF, SR>>(SM, Cf::THREADS, cap);
+  if (e != cudaSuccess) return e;
+  const long tiles = (long)a.O * ((a.C + 2 * Cf::G - 1) / (2 * Cf::G));
+  return pdl_launch(k_colc<L, MODE, PF, SR>, clamp_grid(tiles, cap), Cf::THREADS, SM, st, a);
+}
+template <int L, int MODE, bool PF>
+static cudaError_t run_colc_v(cudaStream_t st, const ColArgs& a) {
+  return a.sym_re ? run_colc_s<L, MODE, PF, true>(st, a) : run_colc_s<L, MODE, PF, false>(st, a);
+}
+
 template <int L, int MODE, bool PF>
 static cudaError_t run_row_v(cudaStream_t st, const RowArgs& a) {
+  if constexpr (UseSplit<L>::value) {
+    return run_rowc_v<L, MODE, PF>(st, a);
+  }
   using Cf = Cfg<L>;
   constexpr size_t SM = RowPlan<L, MODE, PF>::SMEM;
   int cap = 0;
@@ -249,8 +293,9 @@ static cudaError_t run_row_v(cudaStream_t st, const RowArgs& a) {
 template <int L, int MODE>
 static cudaError_t run_row(cudaStream_t st, const RowArgs& a) {
   // pipelined full tiles: n == L/2 and tiles of 2G fibres inside one slice
+  constexpr int G = UseSplit<L>::value ? CCfg<L>::G : Cfg<L>::G;
   if constexpr (Cfg<L>::PF_OK) {
-    if (2 * a.n == L && a.n1 % (2 * Cfg<L>::G) == 0) return run_row_v<L, MODE, true>(st, a);
+    if (2 * a.n == L && a.n1 % (2 * G) == 0) return run_row_v<L, MODE, true>(st, a);
   }
   return run_row_v<L, MODE, false>(st, a);
 }
@@ -268,6 +313,9 @@ static cudaError_t dispatch_row(cudaStream_t st, int L, const RowArgs& a) {
 
 template <int L, int MODE, bool PF>
 static cudaError_t run_col_v(cudaStream_t st, const ColArgs& a) {
+  if constexpr (UseSplit<L>::value) {
+    return run_colc_v<L, MODE, PF>(st, a);
+  }
   using Cf = Cfg<L>;
   constexpr size_t SM = ColPlan<L, PF>::SMEM;
   int cap = 0;
@@ -279,8 +327,9 @@ static cudaError_t run_col_v(cudaStream_t st, const ColArgs& a) {
 
 template <int L, int MODE>
 static cudaError_t run_col(cudaStream_t st, const ColArgs& a) {
+  constexpr int G = UseSplit<L>::value ? CCfg<L>::G : Cfg<L>::G;
   if constexpr (Cfg<L>::PF_OK) {
-    if (2 * a.n == L && a.C % (2 * Cfg<L>::G) == 0) return run_col_v<L, MODE, true>(st, a);
+    if (2 * a.n == L && a.C % (2 * G) == 0) return run_col_v<L, MODE, true>(st, a);
   }
   return run_col_v<L, MODE, false>(st, a);
 }
@@ -306,7 +355,10 @@ cudaError_t launch_row_apply(cudaStream_t st, LaunchCounter* lc, const double* x
   a.n1 = n1;
   a.n = n2;
   a.sym = s2.sym;
+  a.sym_re = s2.sym_re;
   a.tw = s2.tw;
+  a.twh = s2.twh;
+  a.twist = s2.twist;
   a.scale = scale;
   a.tkind = tf.kind == 1 ? 1 : 0;
   a.tc0 = 0.0;  // folded into the x2 symbol (fdg_api.cu ax2s)
@@ -330,7 +382,10 @@ cudaError_t launch_row_s_out(cudaStream_t st, LaunchCounter* lc, const double* w
   a.n1 = n1;
   a.n = n2;
   a.sym = s2.sym;
+  a.sym_re = s2.sym_re;
   a.tw = s2.tw;
+  a.twh = s2.twh;
+  a.twist = s2.twist;
   a.scale = scale;
   a.tkind = tf.kind == 1 ? 1 : 0;
   a.tc0 = 0.0;  // folded into the x2 symbol (fdg_api.cu ax2s)
@@ -359,7 +414,10 @@ cudaError_t launch_row_fused(cudaStream_t st, LaunchCounter* lc, const double* z
   a.n1 = n1;
   a.n = n2;
   a.sym = s2.sym;
+  a.sym_re = s2.sym_re;
   a.tw = s2.tw;
+  a.twh = s2.twh;
+  a.twist = s2.twist;
   a.scale = scale;
   a.tkind = tf.kind == 1 ? 1 : 0;
   a.tc0 = 0.0;
@@ -385,7 +443,10 @@ cudaError_t launch_col_acc(cudaStream_t st, LaunchCounter* lc, const double* x, 
   a.n = n;
   a.C = C;
   a.sym = adjoint ? s.sym_adj : s.sym;
+  a.sym_re = adjoint ? s.sym_adj_re : s.sym_re;
   a.tw = s.tw;
+  a.twh = s.twh;
+  a.twist = s.twist;
   a.scale = scale;
   count(lc);
   return dispatch_col<0>(st, s.L, a);
@@ -404,7 +465,10 @@ cudaError_t launch_col_s_mid(cudaStream_t st, LaunchCounter* lc, const double* p
   a.n = n1;
   a.C = n2;
   a.sym = s1.sym;
+  a.sym_re = s1.sym_re;
   a.tw = s1.tw;
+  a.twh = s1.twh;
+  a.twist = s1.twist;
   a.scale = scale;
   a.inv_m2 = inv_m2;
   a.a1 = a1;

@@ -30,15 +30,33 @@ namespace fdg {
 // Tile configuration for transform length L.
 //   R: complex values per thread, T = L/R threads per lane, G lanes per CTA
 //   (256 threads), DB: double-buffered exchanges, TS: twiddles in smem.
+#ifndef FDG_T256_THREADS
+#define FDG_T256_THREADS 128
+#endif
+#ifndef FDG_T256_MINB
+#define FDG_T256_MINB 3
+#endif
+#ifndef FDG_T256_DB
+#define FDG_T256_DB 0
+#endif
+#ifndef FDG_T512_THREADS
+#define FDG_T512_THREADS 256
+#endif
+#ifndef FDG_T512_MINB
+#define FDG_T512_MINB 2
+#endif
+#ifndef FDG_T512_DB
+#define FDG_T512_DB 1
+#endif
 template <int L>
 struct Cfg {
   static constexpr int R = fft_radix(L);
   static constexpr int T = L / R;
-  static constexpr int G_ = 256 / T;
+  static constexpr int G_ = (L == 256 ? FDG_T256_THREADS : (L == 512 ? FDG_T512_THREADS : 256)) / T;
   static constexpr int G = G_ > 32 ? 32 : (G_ < 2 ? 2 : G_);
   static constexpr int THREADS = G * T;
-  static constexpr int MINB = 2;
-  static constexpr bool DB = L <= 512;
+  static constexpr int MINB = L == 256 ? FDG_T256_MINB : (L == 512 ? FDG_T512_MINB : 2);
+  static constexpr bool DB = L == 256 ? (FDG_T256_DB != 0) : (L == 512 ? (FDG_T512_DB != 0) : L <= 512);
   static constexpr bool TS = L <= 1024;
   static constexpr size_t EXB = (size_t)L * G;  // double2 per exchange buffer
   static constexpr bool PF_OK = L >= 16 && L <= 512;
@@ -136,6 +154,9 @@ struct RowArgs {
   int first;  // d_new = z (first Krylov iteration, no beta term, no x update)
   int upd_x;  // apply x += alpha d_old
   const int* guard;  // speculative PCG iteration: skip the launch when *guard != 0
+  const double2* twh;    // split passes (fdg_conv.cuh): L/2-point twiddles
+  const double2* twist;  // split passes: W_L^j, j < L/2
+  const double* sym_re;  // split passes: real symbol (symmetric factor) or null
 };
 
 // Early exit of a speculatively enqueued PCG kernel (the host enqueues
@@ -352,6 +373,9 @@ struct ColArgs {
   const double* a1;
   RedSlot red;
   const int* guard;
+  const double2* twh;    // split passes (fdg_conv.cuh)
+  const double2* twist;
+  const double* sym_re;
 };
 
 template <bool FULL>
