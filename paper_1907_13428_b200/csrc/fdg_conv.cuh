@@ -29,6 +29,21 @@
 
 namespace fdg {
 
+// timing experiment: FDG_EXP_NOIO drops the global traffic (numerically invalid)
+#ifdef FDG_EXP_NOIO
+#define FDG_IO(x) \
+  do {                        \
+    if (a.scale == 12345.0) { \
+      x;                      \
+    }                         \
+  } while (0)
+#else
+#define FDG_IO(x) \
+  do {            \
+    x;            \
+  } while (0)
+#endif
+
 #ifndef FDG_C512_THREADS
 #define FDG_C512_THREADS 128
 #endif
@@ -41,8 +56,14 @@ namespace fdg {
 #ifndef FDG_C_HOMO
 #define FDG_C_HOMO 1
 #endif
+#ifndef FDG_C_HOMO_COL
+#define FDG_C_HOMO_COL FDG_C_HOMO
+#endif
 #ifndef FDG_C_EPI
 #define FDG_C_EPI 1
+#endif
+#ifndef FDG_C_COLLY
+#define FDG_C_COLLY 2
 #endif
 
 template <int L>
@@ -59,7 +80,8 @@ struct CCfg {
   static constexpr int MINB_COL = L == 512 ? FDG_C512_MINB_COL : 1;
   static constexpr int HR = R / 2;               // output positions per thread
   static constexpr size_t EXB = (size_t)M * G2;  // double2, one exchange buffer
-  static constexpr bool HOMO = FDG_C_HOMO != 0;
+  static constexpr bool HOMO = FDG_C_HOMO != 0;          // rows
+  static constexpr bool HOMO_COL = FDG_C_HOMO_COL != 0;  // columns
   // sub-lane barriers assume T <= 32; the half-row swizzle a power-of-two G
   static constexpr bool OK = T <= 32 && R >= 2 && (R & 1) == 0 && (G & (G - 1)) == 0;
   // exchange | M-point twiddles | twist W_L^j (j < M) | symbol (L, real or
@@ -121,13 +143,14 @@ struct CSmem {
 };
 
 // Thread -> (lane g, half b, sub-lane thread t, sub-lane slot id gs, partner).
-template <int L, bool ROWS>
+template <int L, bool ROWS, bool HOMO_>
 struct CMap {
+  static constexpr bool HOMO = HOMO_;
   int g, b, t, gs, partner;
   __device__ __forceinline__ CMap() {
     using C = CCfg<L>;
     const int tid = threadIdx.x;
-    if constexpr (C::HOMO) {
+    if constexpr (HOMO) {
       b = tid / (C::G * C::T);
       const int r = tid - b * (C::G * C::T);
       if constexpr (ROWS) {
@@ -154,16 +177,14 @@ struct CMap {
     }
   }
   // slot id holding the lane's half-b values
-  __device__ __forceinline__ int half_id(int h) const {
-    return CCfg<L>::HOMO ? h * CCfg<L>::G + g : 2 * g + h;
-  }
+  __device__ __forceinline__ int half_id(int h) const { return HOMO ? h * CCfg<L>::G + g : 2 * g + h; }
 };
 
 // Barrier over the two sub-lanes of every lane.
-template <int L, int LAYOUT>
+template <int L, int LAYOUT, bool HOMO>
 __device__ __forceinline__ void pair_sync() {
   using C = CCfg<L>;
-  if constexpr (LAYOUT != 1 || C::HOMO || C::LT > 32) {
+  if constexpr (LAYOUT != 1 || HOMO || C::LT > 32) {
     __syncthreads();
   } else {
     __syncwarp();
@@ -180,27 +201,34 @@ __device__ __forceinline__ void conv_half(double2 (&v)[CCfg<L>::R], Ex& ex, int 
 #ifdef FDG_EXP_NOCONV
   return;
 #endif
+#ifndef FDG_EXP_NOTWIST
   if (b) {
 #pragma unroll
     for (int m = 0; m < R; ++m) v[m] = cmul(v[m], twist[t + T * m]);
   }
+#endif
   fft_lane<M, R, G2, false, LAYOUT>(v, ex, t, gs, tw);
+#ifndef FDG_EXP_NOSYM
 #pragma unroll
   for (int m = 0; m < R; ++m) v[m] = sym.apply(v[m], 2 * (t + T * m) + b);
+#endif
   fft_lane<M, R, G2, true, LAYOUT>(v, ex, t, gs, tw);
+#ifndef FDG_EXP_NOTWIST
   if (b) {
 #pragma unroll
     for (int m = 0; m < R; ++m) v[m] = cmulc(v[m], twist[t + T * m]);
   }
+#endif
 }
 
 // Adds the two halves: half 0 owns positions t + T m for m < R/2, half 1
 // those for m >= R/2; y[i] is position t + T (i + b R/2).  Each store
 // instruction writes one half-row of both halves (conflict-free).  TRAIL:
 // barrier after the reads (when no other barrier precedes the next scatter).
-template <int L, int LAYOUT, bool TRAIL>
+template <int L, int LAYOUT, bool TRAIL, class Map>
 __device__ __forceinline__ void conv_combine(const double2 (&v)[CCfg<L>::R], double2 (&y)[CCfg<L>::HR], Ex& ex,
-                                             const CMap<L, LAYOUT == 1>& mp) {
+                                             const Map& mp) {
+  constexpr bool HM = Map::HOMO;
   using C = CCfg<L>;
   constexpr int M = C::M, T = C::T, G2 = C::G2, HR = C::HR;
   const int t = mp.t, b = mp.b;
@@ -209,20 +237,20 @@ __device__ __forceinline__ void conv_combine(const double2 (&v)[CCfg<L>::R], dou
   for (int i = 0; i < HR; ++i) y[i] = b ? v[i + HR] : v[i];
   return;
 #endif
-  pair_sync<L, LAYOUT>();  // write-after-read: last inverse-FFT exchange
+  pair_sync<L, LAYOUT, HM>();  // write-after-read: last inverse-FFT exchange
   double2* sm = ex.next();
 #pragma unroll
   for (int i = 0; i < HR; ++i) {
     const double2 val = b ? v[i] : v[i + HR];
     sm[slot<LAYOUT, M, G2>(t + T * (b ? i : i + HR), mp.gs)] = val;
   }
-  pair_sync<L, LAYOUT>();
+  pair_sync<L, LAYOUT, HM>();
 #pragma unroll
   for (int i = 0; i < HR; ++i) {
     const double2 mine = b ? v[i + HR] : v[i];
     y[i] = cadd(mine, sm[slot<LAYOUT, M, G2>(t + T * (i + b * HR), mp.partner)]);
   }
-  if constexpr (TRAIL) pair_sync<L, LAYOUT>();
+  if constexpr (TRAIL) pair_sync<L, LAYOUT, HM>();
 }
 
 // =================================================================== rows
@@ -258,7 +286,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
   double* st_nb2 = st_nb + TILE;
   double* st_vp = S.stage + 2 * TILE;
   double* st_r = S.stage + 3 * TILE;
-  const CMap<L, true> mp;
+  const CMap<L, true, C::HOMO> mp;
   const int g = mp.g, b = mp.b, t = mp.t;
   const int F = a.nt * a.n1;
   const int ntiles = (F + 2 * G - 1) / (2 * G);
@@ -278,8 +306,8 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
   double acc = 0.0;
   if constexpr (PF) {
     if (blockIdx.x < ntiles) {
-      stage_rows(st_in, in0 + (size_t)blockIdx.x * 2 * G * n, TILE);
-      if (MODE == 2 && !first) stage_rows(st_in2, in1 + (size_t)blockIdx.x * 2 * G * n, TILE);
+      FDG_IO(stage_rows(st_in, in0 + (size_t)blockIdx.x * 2 * G * n, TILE));
+      if (MODE == 2 && !first) FDG_IO(stage_rows(st_in2, in1 + (size_t)blockIdx.x * 2 * G * n, TILE));
     }
     cp_async_commit();
   }
@@ -304,8 +332,8 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
             z.y += beta * st_in2[(2 * g + 1) * M + pos];
           }
           if ((m < HR) == (b == 0)) {
-            a.dnew[ra + pos] = z.x;
-            a.dnew[ra + n + pos] = z.y;
+            FDG_IO(a.dnew[ra + pos] = z.x);
+            FDG_IO(a.dnew[ra + n + pos] = z.y);
           }
         }
         v[m] = z;
@@ -315,19 +343,19 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
       tile_nb = a.tkind == 1 && (a.tdir < 0 ? k >= 1 : k + 1 < a.nt);
       if constexpr (SEPI) {
         if (tile_nb) {
-          stage_rows(st_nb, in0 + (size_t)f0 * n + noff, TILE);
-          if (MODE == 2 && !first) stage_rows(st_nb2, in1 + (size_t)f0 * n + noff, TILE);
+          FDG_IO(stage_rows(st_nb, in0 + (size_t)f0 * n + noff, TILE));
+          if (MODE == 2 && !first) FDG_IO(stage_rows(st_nb2, in1 + (size_t)f0 * n + noff, TILE));
         }
         if constexpr (MODE == 1) {
-          stage_rows(st_vp, a.vp + (size_t)f0 * n, TILE);
-          if (a.r) stage_rows(st_r, a.r + (size_t)f0 * n, TILE);
+          FDG_IO(stage_rows(st_vp, a.vp + (size_t)f0 * n, TILE));
+          if (a.r) FDG_IO(stage_rows(st_r, a.r + (size_t)f0 * n, TILE));
         }
       }
       cp_async_commit();  // group E
       const int nxt = tile + gridDim.x;
       if (nxt < ntiles) {
-        stage_rows(st_in, in0 + (size_t)nxt * 2 * G * n, TILE);
-        if (MODE == 2 && !first) stage_rows(st_in2, in1 + (size_t)nxt * 2 * G * n, TILE);
+        FDG_IO(stage_rows(st_in, in0 + (size_t)nxt * 2 * G * n, TILE));
+        if (MODE == 2 && !first) FDG_IO(stage_rows(st_in2, in1 + (size_t)nxt * 2 * G * n, TILE));
       }
       cp_async_commit();  // group I
     } else {
@@ -344,8 +372,8 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
               if (vb) z.y += beta * __ldg(in1 + ra + n + pos);
             }
             if ((m < HR) == (b == 0)) {
-              if (va) a.dnew[ra + pos] = z.x;
-              if (vb) a.dnew[ra + n + pos] = z.y;
+              if (va) FDG_IO(a.dnew[ra + pos] = z.x);
+              if (vb) FDG_IO(a.dnew[ra + n + pos] = z.y);
             }
           }
         }
@@ -387,14 +415,14 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
           }
         }
         if constexpr (MODE == 0 || MODE == 2) {
-          a.out[o] = val;
-          if (MODE == 2 && a.upd_x) a.xs[o] += alpha * __ldg(in1 + o);
+          FDG_IO(a.out[o] = val);
+          if (MODE == 2 && a.upd_x) FDG_IO(a.xs[o] += alpha * __ldg(in1 + o));
         } else {
           const double q = (SEPI ? st_vp[sl] : __ldg(&a.vp[o])) + val;
           if (a.q_out) a.q_out[o] = q;
           if (a.r) {
             const double rn = (SEPI ? st_r[sl] : a.r[o]) - alpha * q;
-            a.r[o] = rn;
+            FDG_IO(a.r[o] = rn);
             acc += rn * rn;
           }
         }
@@ -414,9 +442,14 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
 template <int L, int MODE, bool PF, bool SR>
 struct ColCPlan {
   using C = CCfg<L>;
-  static constexpr int TILE = PF ? 2 * C::G * C::M : 0;
-  // MODE 2: double-buffered input (p stays readable for both epilogues) + u
-  static constexpr int NST = MODE == 2 ? 3 : 1;
+  // exchange layout: 1 = lane-major (sub-lane-local exchanges, __syncwarp),
+  // else interleaved rows (CTA-wide barriers)
+  static constexpr int LY = FDG_C_COLLY == 1 ? 1 : (C::HOMO_COL ? 2 : 0);
+  static constexpr int W = 2 * C::G;              // columns per tile
+  static constexpr int P = LY == 1 ? W + 2 : W;   // staged row pitch (bank spread)
+  static constexpr int TILE = PF ? C::M * P : 0;  // doubles per staged operand
+  // MODE 2: double-buffered p (readable by both epilogues) and u
+  static constexpr int NST = MODE == 2 ? 4 : 1;
   static constexpr size_t SMEM = C::bytes((size_t)TILE * NST, SR);
 };
 
@@ -428,16 +461,16 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
   using Cf = CCfg<L>;
   static_assert(Cf::OK, "split pass configuration");
   constexpr int M = Cf::M, R = Cf::R, T = Cf::T, G = Cf::G, G2 = Cf::G2, HR = Cf::HR;
-  constexpr int LY = Cf::HOMO ? 2 : 0;
-  constexpr int W = 2 * G;
+  using CP = ColCPlan<L, MODE, PF, SR>;
+  constexpr int LY = CP::LY, W = CP::W, P = CP::P;
   extern __shared__ double2 smem_raw[];
   __shared__ double scratch[32];
   CSmem<L, SR> S(smem_raw, a.twh, a.twist, a.sym, a.sym_re);
   pdl_trigger();
   pdl_wait();
   if (paused(a.guard)) return;
-  constexpr int TILE = ColCPlan<L, MODE, PF, SR>::TILE;
-  const CMap<L, false> mp;
+  constexpr int TILE = CP::TILE;
+  const CMap<L, LY == 1, Cf::HOMO_COL> mp;
   const int g = mp.g, b = mp.b, t = mp.t;
   const int n = a.n, C = a.C;
   const int ncb = (C + W - 1) / W;
@@ -445,13 +478,12 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
   // staged column tile [pos][W] of `src` for tile index tl
   auto stage_tile = [&](double* dst, const double* src, int tl) {
     const int ot = tl / ncb;
-    stage_cols<W>(dst, src + (size_t)ot * n * C + (size_t)(tl - ot * ncb) * W, n, C);
+    stage_cols<W, P>(dst, src + (size_t)ot * n * C + (size_t)(tl - ot * ncb) * W, n, C);
   };
-  double* st_u = S.stage + 2 * TILE;  // MODE 2
   if constexpr (PF) {
     if (blockIdx.x < ntiles) {
-      stage_tile(S.stage, a.x, blockIdx.x);
-      if constexpr (MODE == 2) stage_tile(st_u, a.acc, blockIdx.x);
+      FDG_IO(stage_tile(S.stage, a.x, blockIdx.x));
+      if constexpr (MODE == 2) FDG_IO(stage_tile(S.stage + 2 * TILE, a.acc, blockIdx.x));
     }
     cp_async_commit();
   }
@@ -466,14 +498,18 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
     const size_t base = (size_t)o * n * C + c;
     const int nxt = tile + gridDim.x;
     double* st_in = S.stage + buf * TILE;
+    const double* st_u = S.stage + (2 + buf) * TILE;  // MODE 2
     double2 v[R];
     if constexpr (PF) {
       cp_async_wait<0>();
       __syncthreads();
 #pragma unroll
-      for (int m = 0; m < R; ++m) v[m] = *reinterpret_cast<const double2*>(st_in + (t + m * T) * W + 2 * g);
+      for (int m = 0; m < R; ++m) v[m] = *reinterpret_cast<const double2*>(st_in + (t + m * T) * P + 2 * g);
       if constexpr (MODE != 2) __syncthreads();  // single input buffer
-      if (nxt < ntiles) stage_tile(S.stage + (buf ^ (MODE == 2)) * TILE, a.x, nxt);
+      if (nxt < ntiles) {
+        FDG_IO(stage_tile(S.stage + (buf ^ (MODE == 2)) * TILE, a.x, nxt));
+        if constexpr (MODE == 2) FDG_IO(stage_tile(S.stage + (2 + (buf ^ 1)) * TILE, a.acc, nxt));
+      }
       cp_async_commit();
     } else {
 #pragma unroll
@@ -494,7 +530,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
         const size_t o2 = base + (size_t)pos * C;
         double2 acc = make_double2(0.0, 0.0);
         if (a.acc) acc = col_get<PF>(a.acc + o2, C, c);
-        col_put<PF>(a.out + o2, C, c, make_double2(acc.x + a.scale * y[i].x, acc.y + a.scale * y[i].y));
+        FDG_IO(col_put<PF>(a.out + o2, C, c, make_double2(acc.x + a.scale * y[i].x, acc.y + a.scale * y[i].y)));
       }
     } else {
       // S mid pass: Bp = u + scale L1 p; w = Bp / m2[o] (-> a.w, and the
@@ -505,14 +541,14 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
         const int pos = t + T * (i + b * HR);
         if (PF || (pos < n && vc)) {
           const size_t o2 = base + (size_t)pos * C;
-          const double2 u = PF ? *reinterpret_cast<const double2*>(st_u + pos * W + 2 * g) : col_get<PF>(a.acc + o2, C, c);
-          const double2 pv = PF ? *reinterpret_cast<const double2*>(st_in + pos * W + 2 * g) : col_get<PF>(a.x + o2, C, c);
+          const double2 u = PF ? *reinterpret_cast<const double2*>(st_u + pos * P + 2 * g) : col_get<PF>(a.acc + o2, C, c);
+          const double2 pv = PF ? *reinterpret_cast<const double2*>(st_in + pos * P + 2 * g) : col_get<PF>(a.x + o2, C, c);
           const double bx = u.x + a.scale * y[i].x;
           const double by = u.y + a.scale * y[i].y;
           const double wx = bx * im2, wy = vb ? by * im2 : 0.0;
           e += a1 * pv.x * pv.x + wx * bx;
           if (vb) e += a1 * pv.y * pv.y + wy * by;
-          col_put<PF>(a.w + o2, C, c, make_double2(wx, wy));
+          FDG_IO(col_put<PF>(a.w + o2, C, c, make_double2(wx, wy)));
           y[i] = make_double2(wx, wy);
         } else {
           y[i] = make_double2(0.0, 0.0);
@@ -520,15 +556,11 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
       }
       // both halves need all of w: each writes its positions into its own
       // slot column, then reads the lane's full column pair
-      __syncthreads();  // write-after-read: combine (and every read of st_u)
-      if constexpr (PF) {
-        if (nxt < ntiles) stage_tile(st_u, a.acc, nxt);
-        cp_async_commit();
-      }
+      pair_sync<L, LY, Cf::HOMO_COL>();  // write-after-read: combine
       double2* sm = S.ex.next();
 #pragma unroll
       for (int i = 0; i < HR; ++i) sm[slot<LY, M, G2>(t + T * (i + b * HR), mp.gs)] = y[i];
-      __syncthreads();
+      pair_sync<L, LY, Cf::HOMO_COL>();
       const int id0 = mp.half_id(0), id1 = mp.half_id(1);
 #pragma unroll
       for (int m = 0; m < R; ++m) v[m] = sm[slot<LY, M, G2>(t + T * m, m < HR ? id0 : id1)];
@@ -539,8 +571,8 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
         const int pos = t + T * (i + b * HR);
         if (!PF && (pos >= n || !vc)) continue;
         const size_t o2 = base + (size_t)pos * C;
-        const double2 pv = PF ? *reinterpret_cast<const double2*>(st_in + pos * W + 2 * g) : col_get<PF>(a.x + o2, C, c);
-        col_put<PF>(a.out + o2, C, c, make_double2(a.scale * y[i].x + a1 * pv.x, a.scale * y[i].y + a1 * pv.y));
+        const double2 pv = PF ? *reinterpret_cast<const double2*>(st_in + pos * P + 2 * g) : col_get<PF>(a.x + o2, C, c);
+        FDG_IO(col_put<PF>(a.out + o2, C, c, make_double2(a.scale * y[i].x + a1 * pv.x, a.scale * y[i].y + a1 * pv.y)));
       }
     }
   }

@@ -35,6 +35,17 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
 }
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
 
+// 1/x for finite x > 0 without the IEEE division slow path: MUFU reciprocal
+// seed and two Newton steps (error within 2 ulp).
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 // Multiply by W_R^q = exp(-/+ 2 pi i q / R) for compile-time (R, q).
 template <int R, int Q, bool INV>
 __device__ __forceinline__ double2 mul_wq(double2 x) {

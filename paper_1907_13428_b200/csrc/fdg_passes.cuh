@@ -111,13 +111,13 @@ __device__ __forceinline__ void stage_rows(double* dst, const double* src, int n
   for (int i = 2 * threadIdx.x; i < nd; i += 2 * blockDim.x) cp_async16(dst + i, src + i);
 }
 // CTA-cooperative copy of a column tile: n positions x W doubles (W even),
-// source row stride C doubles -> dense [pos][W] in shared memory.
-template <int W>
+// source row stride C doubles -> [pos][P] in shared memory (pitch P >= W).
+template <int W, int P = W>
 __device__ __forceinline__ void stage_cols(double* dst, const double* src, int n, int C) {
   constexpr int CH = W / 2;  // 16-byte chunks per position
   for (int i = threadIdx.x; i < n * CH; i += blockDim.x) {
     const int pos = i / CH, j = i - pos * CH;
-    cp_async16(dst + pos * W + 2 * j, src + (size_t)pos * C + 2 * j);
+    cp_async16(dst + pos * P + 2 * j, src + (size_t)pos * C + 2 * j);
   }
 }
 
@@ -719,7 +719,7 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(doub
       const double lsa = pt.base + (bax * bax + bay * bay) * pt.inv_m2;
       const double lsb = pt.base + (bbx * bbx + bby * bby) * pt.inv_m2;
       // one reciprocal for both columns
-      const double inv = pt.inv_total / (lsa * lsb);
+      const double inv = pt.inv_total * frcp(lsa * lsb);
       v[m] = make_double2(h.x * (lsb * inv), h.y * (lsa * inv));
     }
     fft_lane<N, R, G, false>(v, S.ex, t, g, S.tw);
