@@ -103,6 +103,16 @@ fdg_status fdg_pc_solve(fdg_pc pc, const double* r_dev, double* z_dev);
 fdg_status fdg_pc_solve_host(fdg_pc pc, const double* r, size_t n_r, double* z, size_t n_z);
 /* lam_S materialized on the host (tests; circulant.hpp:47) */
 fdg_status fdg_pc_lam_s_host(fdg_pc pc, double* out);
+/* 2-level spatial T. Chan preconditioner of A = I (x) T_x + T_y (x) I applied per
+ * time slice (BASELINE C1 operator microbenchmark; the reference ships only the
+ * 3-level ADMM form, circulant.cpp:28-90): z = F^-1 (F r / (lam_x1[i] + lam_x2[j])),
+ * any level sizes <= 1024 (Bluestein).  Eigenvalues complex interleaved and real
+ * (symmetric factors).  Solved through fdg_pc_solve / fdg_pc_solve_host. */
+fdg_status fdg_pc2_create(fdg_ctx ctx, int n_t, int n_x1, int n_x2, const double* lam_x1,
+                          const double* lam_x2, fdg_pc* out);
+/* Same, with lam from the T. Chan circulants (circulant.cpp:10-26) of the
+ * operator's spatial factors. */
+fdg_status fdg_pc2_assemble(fdg_op op, fdg_pc* out);
 
 /* ---------------------------------------------------------------- ADMM */
 /* AdmmConfig (admm.hpp:14-26) + ProblemSpec bounds/gamma (problem.hpp:15-26). */

@@ -631,3 +631,24 @@ def baseline_problem(name: str, shape: Shape | None = None):
     c.update(time=time, r1=r1, r2=r2, psi=psi, rho=1.0, delta=1.0, krylov_tol=1e-8,
              tol_primal=1e-6, max_inner=400)
     return c
+
+
+def spatial_precond_solve(shape, lam_x1, lam_x2, r):
+    """BASELINE C1 preconditioner restated with numpy (pocketfft): per time
+    slice z = F^-1 (F r / (lam_x1[i] + lam_x2[j])), the 2-level T. Chan
+    circulant of A = I (x) T_x + T_y (x) I.  Independent of
+    the GPU's Bluestein Hartley passes."""
+    nt, n1, n2 = shape
+    R = np.asarray(r, dtype=np.float64).reshape(nt, n1, n2)
+    D = np.asarray(lam_x1)[:, None] + np.asarray(lam_x2)[None, :]
+    Z = np.fft.ifft2(np.fft.fft2(R, axes=(1, 2)) / D, axes=(1, 2))
+    return np.ascontiguousarray(Z.real).ravel()
+
+
+def circulant_dense(first_col):
+    """Dense circulant with the given first column (C[i, j] = c[(i - j) mod n])."""
+    c = np.asarray(first_col)
+    n = c.size
+    idx = (np.arange(n)[:, None] - np.arange(n)[None, :]) % n
+    return c[idx]
+

@@ -6,8 +6,9 @@ C ABI in include/fdg.h.  All arithmetic runs in lib/libfdg.so on the GPU; the
 import fails if the library is missing (no CPU fallback).
 """
 from .api import (  # noqa: F401
-    Context, ConstraintOperator, CirculantPreconditioner, AdmmConfig, AdmmDriver, IterRecord,
+    Context, ConstraintOperator, CirculantPreconditioner, SpatialPreconditioner,
+    assemble_spatial_precond, AdmmConfig, AdmmDriver, IterRecord,
     PcgResult, assemble_precond, solve, frac_coeffs, build_riesz, build_caputo, tchan, randn,
     implicit_euler, FdgError,
 )
-from .workloads import baseline_config, synthetic_ybar, make_problem  # noqa: F401
+from .workloads import baseline_config, synthetic_ybar, make_problem, make_c1, c1_factors  # noqa: F401

@@ -82,6 +82,8 @@ _sig("fdg_pc_destroy", _st, _vp)
 _sig("fdg_pc_solve", _st, _vp, _vp, _vp)
 _sig("fdg_pc_solve_host", _st, _vp, _dp, C.c_size_t, _dp, C.c_size_t)
 _sig("fdg_pc_lam_s_host", _st, _vp, _dp)
+_sig("fdg_pc2_create", _st, _vp, C.c_int, C.c_int, C.c_int, _dp, _dp, C.POINTER(_vp))
+_sig("fdg_pc2_assemble", _st, _vp, C.POINTER(_vp))
 _sig("fdg_admm_create", _st, _vp, _vp, C.POINTER(AdmmDesc), _dp, C.POINTER(_vp))
 _sig("fdg_admm_destroy", _st, _vp)
 _sig("fdg_admm_step", _st, _vp, C.POINTER(IterRecord))

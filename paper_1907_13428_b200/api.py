@@ -211,6 +211,32 @@ def assemble_precond(op: ConstraintOperator, rho: float, delta: float, gamma: fl
     return CirculantPreconditioner(h.value, op.shape, op.ctx, keep=op)
 
 
+class SpatialPreconditioner(CirculantPreconditioner):
+    """Per-slice 2-level T. Chan preconditioner of A = I (x) T_x + T_y (x) I
+    (BASELINE C1): z = F^-1 (F r / (lam_x1[i] + lam_x2[j])) slice by slice,
+    any level sizes up to 1024 (Bluestein Hartley passes)."""
+
+    @classmethod
+    def from_eigs(cls, n_t, lam_x1, lam_x2, ctx: Context | None = None):
+        ctx = ctx or default_context()
+        arrs = [_f64(np.stack([np.real(v), np.imag(v)], -1).ravel()) for v in (lam_x1, lam_x2)]
+        h = C.c_void_p()
+        shape = (int(n_t), len(lam_x1), len(lam_x2))
+        check(lib.fdg_pc2_create(ctx.h, *shape, *[_ptr(a) for a in arrs], C.byref(h)))
+        return cls(h.value, shape, ctx)
+
+    def lam_s(self):
+        raise ValueError("lam_S exists only for the 3-level CirculantPreconditioner")
+
+
+def assemble_spatial_precond(op: ConstraintOperator) -> SpatialPreconditioner:
+    """2-level T. Chan preconditioner from the operator's spatial factors
+    (circulant.cpp:10-26 per level)."""
+    h = C.c_void_p()
+    check(lib.fdg_pc2_assemble(op.h, C.byref(h)))
+    return SpatialPreconditioner(h.value, op.shape, op.ctx, keep=op)
+
+
 # ------------------------------------------------------------------ ADMM
 @dataclass
 class AdmmConfig:

@@ -18,6 +18,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/fdg.h"
@@ -170,6 +171,48 @@ std::vector<double> embed_symbol_full(const std::vector<double>& col, const std:
       const int idx = (int)(((long long)f * k) % L);
       re += v * cs[idx];
       im += v * sn[idx];
+    }
+    out[2 * f] = (double)re;
+    out[2 * f + 1] = (double)im;
+  }
+  return out;
+}
+
+// Bluestein chirp c_m = exp(i pi m^2 / n), m < n (exact m^2 mod 2n).
+std::vector<double> chirp_table(int n) {
+  std::vector<double> c(2 * (size_t)n);
+  for (int m = 0; m < n; ++m) {
+    const long long q = ((long long)m * m) % (2LL * n);
+    const long double a = kPi * (long double)q / (long double)n;
+    c[2 * m] = (double)cosl(a);
+    c[2 * m + 1] = (double)sinl(a);
+  }
+  return c;
+}
+
+// Length-L circulant-embedding spectrum of the symmetric complex Toeplitz
+// matrix T_kj = c_{k-j} (chirp convolution): sum_{|m| < n} c_m W_L^(f m).
+std::vector<double> chirp_symbol(int n, int L) {
+  std::vector<long double> cs(L), sn(L), cr(n), ci(n);
+  for (int k = 0; k < L; ++k) {
+    const long double a = -2.0L * kPi * (long double)k / (long double)L;
+    cs[k] = cosl(a);
+    sn[k] = sinl(a);
+  }
+  for (int m = 0; m < n; ++m) {
+    const long long q = ((long long)m * m) % (2LL * n);
+    const long double a = kPi * (long double)q / (long double)n;
+    cr[m] = cosl(a);
+    ci[m] = sinl(a);
+  }
+  std::vector<double> out(2 * (size_t)L);
+  for (int f = 0; f < L; ++f) {
+    long double re = 0.0L, im = 0.0L;
+    for (int m = -(n - 1); m < n; ++m) {
+      const int am = m < 0 ? -m : m;
+      const int idx = (int)((((long long)f * m) % L + L) % L);
+      re += cr[am] * cs[idx] - ci[am] * sn[idx];
+      im += cr[am] * sn[idx] + ci[am] * cs[idx];
     }
     out[2 * f] = (double)re;
     out[2 * f + 1] = (double)im;
@@ -363,15 +406,49 @@ void op_apply_dev(fdg_op_s* op, const double* x, double* out, bool adjoint) {
 // ================================================================== pc
 struct fdg_pc_s {
   fdg_ctx ctx = nullptr;
+  int kind = 3;  // 3: ADMM 3-level lambda_S (circulant.cpp); 2: per-slice 2-level spatial (BASELINE C1)
   int nt = 0, n1 = 0, n2 = 0;
   double psi = 1.0, rho = 1.0, delta = 1.0, gamma = 1.0;
   DevBuf lt, l1, l2, twt, tw1, tw2;
   DevBuf work;  // N doubles (standalone solve)
   PcTables tab;
+  // kind 2 (Bluestein passes, fdg_kernels.cu k_bs_*): chirps, real eigenvalues,
+  // chirp convolution axes and two work buffers
+  DevBuf c1, c2, lam1, lam2, bu, bv;
+  DevBuf s1, t1, th1, ts1, s2, t2, th2, ts2;
+  AxisSym bs1, bs2;
+  int P2 = 0;
   size_t N() const { return (size_t)nt * n1 * n2; }
 };
 
 namespace {
+
+// 2-level spatial preconditioner (BASELINE C1): per time slice
+// z = F^-1 (F r / (lam1[i] + lam2[j])) with F the n1 x n2 DFT, evaluated as
+// Hartley transforms (the eigenvalues of the T. Chan circulants of symmetric
+// factors are real and even) of any size by Bluestein: x2 forward, x1
+// forward + divide + x1 inverse, x2 inverse, 9 passes.
+void pc2_apply_dev(fdg_pc_s* pc, const double* r, double* z) {
+  cudaStream_t st = pc->ctx->stream;
+  LaunchCounter* lc = &pc->ctx->lc;
+  const long F = (long)pc->nt * pc->n1;
+  const int Fp = (int)(F + (F & 1));
+  const int n1 = pc->n1, n2 = pc->n2, P2 = pc->P2;
+  const double2* c1 = pc->c1.c();
+  const double2* c2 = pc->c2.c();
+  double* u = pc->bu.d();
+  double* v = pc->bv.d();
+  TimeFactor none;
+  ck(fdg::launch_bs_pre_rows(st, lc, r, u, F, n2, c2), "pc2 x2 pre");
+  ck(fdg::launch_row_apply(st, lc, u, v, 1, Fp, n2, pc->bs2, 1.0 / pc->bs2.L, none, 1.0, false), "pc2 x2 conv");
+  ck(fdg::launch_bs_rows_to_cols(st, lc, v, u, F, n1, n2, P2, c2, c1), "pc2 x2 post");
+  ck(fdg::launch_col_acc(st, lc, u, nullptr, v, pc->nt, n1, P2, pc->bs1, 1.0 / pc->bs1.L, false), "pc2 x1 conv");
+  ck(fdg::launch_bs_cols_filter(st, lc, v, u, pc->nt, n1, n2, P2, c1, pc->lam1.d(), pc->lam2.d()), "pc2 divide");
+  ck(fdg::launch_col_acc(st, lc, u, nullptr, v, pc->nt, n1, P2, pc->bs1, 1.0 / pc->bs1.L, false), "pc2 x1 conv");
+  ck(fdg::launch_bs_cols_to_rows(st, lc, v, u, F, n1, n2, P2, c1, c2), "pc2 x1 post");
+  ck(fdg::launch_row_apply(st, lc, u, v, 1, Fp, n2, pc->bs2, 1.0 / pc->bs2.L, none, 1.0, false), "pc2 x2 conv");
+  ck(fdg::launch_bs_post_rows(st, lc, v, z, F, n2, c2, 1.0 / ((double)n1 * n2)), "pc2 x2 post");
+}
 
 // z = S~^{-1} r via Hartley passes x2, x1, t(+divide), x1, x2.
 // h may alias z (not r).  rdot != null: reduce r.z into red.
@@ -954,6 +1031,81 @@ fdg_status fdg_pc_assemble(fdg_op op, double rho, double delta, double gamma, fd
   });
 }
 
+namespace {
+void build_chirp_axis(fdg_pc_s* pc, AxisSym& ax, DevBuf& sym, DevBuf& tw, DevBuf& twh, DevBuf& tws, int n) {
+  const int L = std::max(2, pow2_ceil(2L * n - 1));
+  if (L > 2048) fail(FDG_EUNSUPPORTED, "fdg: 2-level preconditioner level size " + std::to_string(n) + " > 1024");
+  cudaStream_t st = pc->ctx->stream;
+  ax.n = n;
+  ax.L = L;
+  upload(sym, chirp_symbol(n, L), st);
+  upload(tw, stockham_twiddles(L), st);
+  upload(twh, stockham_twiddles(std::max(1, L / 2)), st);
+  std::vector<double> twist = twiddles(L);
+  twist.resize(2 * (size_t)std::max(1, L / 2));
+  upload(tws, twist, st);
+  ax.sym = ax.sym_adj = sym.c();
+  ax.tw = tw.c();
+  ax.twh = twh.c();
+  ax.twist = tws.c();
+}
+
+fdg_pc_s* make_pc2(fdg_ctx ctx, int nt, int n1, int n2, const double* l1, const double* l2) {
+  if (nt < 1 || n1 < 1 || n2 < 1) fail(FDG_EINVAL, "2-level preconditioner: sizes must be positive");
+  std::vector<double> r1(n1), r2(n2);
+  for (auto [lam, n, out] : {std::tuple{l1, n1, &r1}, std::tuple{l2, n2, &r2}}) {
+    double mx = 0.0, im = 0.0;
+    for (int i = 0; i < n; ++i) {
+      mx = std::max(mx, std::hypot(lam[2 * i], lam[2 * i + 1]));
+      im = std::max(im, std::abs(lam[2 * i + 1]));
+      (*out)[i] = lam[2 * i];
+    }
+    if (im > 1e-10 * std::max(mx, 1e-300))
+      fail(FDG_EUNSUPPORTED, "fdg: 2-level preconditioner needs real eigenvalues (symmetric factors)");
+  }
+  auto pc = std::make_unique<fdg_pc_s>();
+  pc->ctx = ctx;
+  pc->kind = 2;
+  pc->nt = nt;
+  pc->n1 = n1;
+  pc->n2 = n2;
+  pc->P2 = n2 + (n2 & 1);
+  cudaStream_t st = ctx->stream;
+  upload(pc->lam1, r1, st);
+  upload(pc->lam2, r2, st);
+  upload(pc->c1, chirp_table(n1), st);
+  upload(pc->c2, chirp_table(n2), st);
+  build_chirp_axis(pc.get(), pc->bs1, pc->s1, pc->t1, pc->th1, pc->ts1, n1);
+  build_chirp_axis(pc.get(), pc->bs2, pc->s2, pc->t2, pc->th2, pc->ts2, n2);
+  const size_t F = (size_t)nt * n1, Fp = F + (F & 1);
+  const size_t words = std::max(Fp * n2, F * pc->P2);
+  pc->bu.alloc(sizeof(double) * words);
+  pc->bv.alloc(sizeof(double) * words);
+  ctx->ensure_partials(fdg::max_partials_needed(1, (int)Fp, pc->P2));
+  return pc.release();
+}
+}  // namespace
+
+fdg_status fdg_pc2_create(fdg_ctx ctx, int nt, int n1, int n2, const double* lam_x1, const double* lam_x2,
+                          fdg_pc* out) {
+  return guard([&] {
+    check_ctx(ctx);
+    if (!lam_x1 || !lam_x2 || !out) fail(FDG_EINVAL, "fdg_pc2_create: null argument");
+    *out = make_pc2(ctx, nt, n1, n2, lam_x1, lam_x2);
+  });
+}
+
+fdg_status fdg_pc2_assemble(fdg_op op, fdg_pc* out) {
+  return guard([&] {
+    if (!op || !out) fail(FDG_EINVAL, "fdg_pc2_assemble: null argument");
+    check_ctx(op->ctx);
+    std::vector<double> l1(2 * (size_t)op->n1), l2(2 * (size_t)op->n2);
+    tchan_host(op->n1, op->c1.data(), op->r1.data(), nullptr, l1.data());
+    tchan_host(op->n2, op->c2.data(), op->r2.data(), nullptr, l2.data());
+    *out = make_pc2(op->ctx, op->nt, op->n1, op->n2, l1.data(), l2.data());
+  });
+}
+
 fdg_status fdg_pc_destroy(fdg_pc pc) {
   return guard([&] {
     if (pc) {
@@ -969,7 +1121,10 @@ fdg_status fdg_pc_solve(fdg_pc pc, const double* r, double* z) {
     if (!pc) fail(FDG_EINVAL, "precond_solve: null preconditioner");
     pc->ctx->set_device();
     if (r == z) fail(FDG_EINVAL, "precond_solve: r and z must not alias");
-    pc_apply_dev(pc, r, z, z, nullptr, RedSlot{});
+    if (pc->kind == 2)
+      pc2_apply_dev(pc, r, z);
+    else
+      pc_apply_dev(pc, r, z, z, nullptr, RedSlot{});
   });
 }
 
@@ -981,7 +1136,10 @@ fdg_status fdg_pc_solve_host(fdg_pc pc, const double* r, size_t n_r, double* z, 
     cudaStream_t st = pc->ctx->stream;
     DevBuf dr(sizeof(double) * n_r), dz(sizeof(double) * n_z);
     ck(cudaMemcpyAsync(dr.p, r, sizeof(double) * n_r, cudaMemcpyHostToDevice, st), "H2D");
-    pc_apply_dev(pc, dr.d(), dz.d(), dz.d(), nullptr, RedSlot{});
+    if (pc->kind == 2)
+      pc2_apply_dev(pc, dr.d(), dz.d());
+    else
+      pc_apply_dev(pc, dr.d(), dz.d(), dz.d(), nullptr, RedSlot{});
     ck(cudaMemcpyAsync(z, dz.p, sizeof(double) * n_z, cudaMemcpyDeviceToHost, st), "D2H");
     ck(cudaStreamSynchronize(st), "sync");
   });
@@ -990,6 +1148,7 @@ fdg_status fdg_pc_solve_host(fdg_pc pc, const double* r, size_t n_r, double* z, 
 fdg_status fdg_pc_lam_s_host(fdg_pc pc, double* out) {
   return guard([&] {
     if (!pc) fail(FDG_EINVAL, "null preconditioner");
+    if (pc->kind != 3) fail(FDG_EINVAL, "lam_S exists only for the 3-level CirculantPreconditioner");
     std::vector<double> lt(2 * (size_t)pc->nt), l1(2 * (size_t)pc->n1), l2(2 * (size_t)pc->n2);
     pc->ctx->set_device();
     ck(cudaMemcpy(lt.data(), pc->lt.p, lt.size() * 8, cudaMemcpyDeviceToHost), "D2H");
@@ -1011,6 +1170,7 @@ fdg_status fdg_admm_create(fdg_op op, fdg_pc pc, const fdg_admm_desc* desc, cons
   return guard([&] {
     if (!op || !pc || !desc) fail(FDG_EINVAL, "fdg_admm_create: null argument");
     if (op->ctx != pc->ctx) fail(FDG_EINVAL, "fdg_admm_create: operator and preconditioner on different contexts");
+    if (pc->kind != 3) fail(FDG_EINVAL, "fdg_admm_create: the ADMM solve needs the 3-level CirculantPreconditioner");
     if (op->nt != pc->nt || op->n1 != pc->n1 || op->n2 != pc->n2)
       fail(FDG_EINVAL, "fdg_admm_create: operator/preconditioner shape mismatch");
     const fdg_admm_desc& d = *desc;

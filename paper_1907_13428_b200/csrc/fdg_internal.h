@@ -154,6 +154,20 @@ cudaError_t launch_objective(cudaStream_t st, LaunchCounter* lc, const double* y
                              const double* v, const double* diag_j, const double* diag_j2,
                              size_t slice, size_t N, RedSlot red);
 
+// Bluestein stages of the 2-level spatial preconditioner (fdg_kernels.cu).
+// F = nt * n1 real rows; row-pair buffers are [F rounded up to even][n2],
+// column-pair buffers [nt][n1][P2] with P2 = n2 rounded up to even.
+cudaError_t launch_bs_pre_rows(cudaStream_t st, LaunchCounter* lc, const double* in, double* out, long F, int n2,
+                               const double2* c2);
+cudaError_t launch_bs_rows_to_cols(cudaStream_t st, LaunchCounter* lc, const double* v, double* u, long F, int n1,
+                                   int n2, int P2, const double2* c2, const double2* c1);
+cudaError_t launch_bs_cols_filter(cudaStream_t st, LaunchCounter* lc, const double* v, double* u, int nt, int n1,
+                                  int n2, int P2, const double2* c1, const double* lam1, const double* lam2);
+cudaError_t launch_bs_cols_to_rows(cudaStream_t st, LaunchCounter* lc, const double* v, double* u, long F, int n1,
+                                   int n2, int P2, const double2* c1, const double2* c2);
+cudaError_t launch_bs_post_rows(cudaStream_t st, LaunchCounter* lc, const double* v, double* z, long F, int n2,
+                                const double2* c2, double scale);
+
 // Grid of the reduction-bearing kernels (to size partial buffers).
 size_t max_partials_needed(int nt, int n1, int n2);
 

@@ -681,6 +681,172 @@ cudaError_t launch_objective(cudaStream_t st, LaunchCounter* lc, const double* y
   return cudaGetLastError();
 }
 
+// ============================================================== Bluestein
+// Non-power-of-two Hartley transforms of the 2-level spatial preconditioner
+// (BASELINE C1, fdg_api.cu pc2_apply_dev).  Z = DFT_n(a + ib) by Bluestein,
+//   Z_k = conj(c_k) sum_j c_{k-j} conj(c_j) z_j,   c_m = exp(i pi m^2 / n),
+// i.e. a chirp pre-multiply, a Toeplitz convolution with the chirp (the
+// row / column pass kernels with a complex symbol) and a chirp post-multiply;
+// the Hartley transforms of a and b follow from Z_k and Z_{n-k}
+// (fdg_fft.cuh hartley_split).  Real fibres travel in pairs: rows 2q, 2q+1
+// (x2 stage, row pitch n2) or columns 2p, 2p+1 (x1 stage, row pitch P2 =
+// n2 rounded up to even) are the real and imaginary parts of one lane.
+namespace {
+__device__ __forceinline__ double2 ld_pair(const double* p) { return *reinterpret_cast<const double2*>(p); }
+}  // namespace
+
+// x2 pre: out[2q][k] + i out[2q+1][k] = (in[2q][k] + i in[2q+1][k]) conj(c2[k])
+__global__ void k_bs_pre_rows(const double* in, double* out, long F, int n2, const double2* c2) {
+  const long Q = (F + 1) / 2;
+  GRID_STRIDE(e, (size_t)Q * n2) {
+    const long q = (long)(e / n2);
+    const int k = (int)(e - (size_t)q * n2);
+    const long f0 = 2 * q, f1 = 2 * q + 1;
+    const double a = in[f0 * n2 + k], b = f1 < F ? in[f1 * n2 + k] : 0.0;
+    const double2 z = cmulc(make_double2(a, b), c2[k]);
+    out[f0 * n2 + k] = z.x;
+    out[f1 * n2 + k] = z.y;
+  }
+}
+
+// x2 post (forward) + x1 pre: v [Fp][n2] -> u [nt][n1][P2]
+__global__ void k_bs_rows_to_cols(const double* v, double* u, long F, int n1, int n2, int P2, const double2* c2,
+                                  const double2* c1) {
+  const long Q = (F + 1) / 2;
+  const int Pp = P2 / 2;
+  GRID_STRIDE(e, (size_t)Q * Pp) {
+    const long q = (long)(e / Pp);
+    const int p = (int)(e - (size_t)q * Pp);
+    const double* r0 = v + 2 * q * n2;
+    const double* r1 = r0 + n2;
+    double2 h[2];  // h[j] = (row 2q, row 2q+1) Hartley values at column 2p + j
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int k = 2 * p + j;
+      if (k < n2) {
+        const int km = k == 0 ? 0 : n2 - k;
+        const double2 Z = cmulc(make_double2(r0[k], r1[k]), c2[k]);
+        const double2 Zm = cmulc(make_double2(r0[km], r1[km]), c2[km]);
+        h[j] = hartley_split(Z, Zm);
+      } else {
+        h[j] = make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const long f = 2 * q + s;
+      if (f >= F) break;
+      const long o = f / n1;
+      const int i = (int)(f - o * n1);
+      const double2 z = s ? make_double2(h[0].y, h[1].y) : make_double2(h[0].x, h[1].x);
+      const double2 w = cmulc(z, c1[i]);
+      *reinterpret_cast<double2*>(u + (o * n1 + i) * P2 + 2 * p) = w;
+    }
+  }
+}
+
+// x1 post (forward) + 1/(lam1[i] + lam2[j]) + x1 pre (inverse): [nt][n1][P2] -> same
+__global__ void k_bs_cols_filter(const double* v, double* u, int nt, int n1, int n2, int P2, const double2* c1,
+                                 const double* lam1, const double* lam2) {
+  const int Pp = P2 / 2;
+  GRID_STRIDE(e, (size_t)nt * n1 * Pp) {
+    const long row = (long)(e / Pp);  // o * n1 + i
+    const int p = (int)(e - (size_t)row * Pp);
+    const long o = row / n1;
+    const int i = (int)(row - o * n1);
+    const int im = i == 0 ? 0 : n1 - i;
+    const double2 Z = cmulc(ld_pair(v + row * P2 + 2 * p), c1[i]);
+    const double2 Zm = cmulc(ld_pair(v + (o * n1 + im) * P2 + 2 * p), c1[im]);
+    double2 h = hartley_split(Z, Zm);
+    h.x /= lam1[i] + lam2[2 * p];
+    h.y = 2 * p + 1 < n2 ? h.y / (lam1[i] + lam2[2 * p + 1]) : 0.0;
+    *reinterpret_cast<double2*>(u + row * P2 + 2 * p) = cmulc(h, c1[i]);
+  }
+}
+
+// x1 post (inverse) + x2 pre (inverse): v [nt][n1][P2] -> u [Fp][n2]
+__global__ void k_bs_cols_to_rows(const double* v, double* u, long F, int n1, int n2, int P2, const double2* c1,
+                                  const double2* c2) {
+  const long Q = (F + 1) / 2;
+  const int Pp = P2 / 2;
+  GRID_STRIDE(e, (size_t)Q * Pp) {
+    const long q = (long)(e / Pp);
+    const int p = (int)(e - (size_t)q * Pp);
+    double2 h[2];  // h[s] = (column 2p, column 2p+1) Hartley values of row 2q + s
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const long f = 2 * q + s;
+      if (f < F) {
+        const long o = f / n1;
+        const int i = (int)(f - o * n1);
+        const int im = i == 0 ? 0 : n1 - i;
+        const double2 Z = cmulc(ld_pair(v + f * P2 + 2 * p), c1[i]);
+        const double2 Zm = cmulc(ld_pair(v + (o * n1 + im) * P2 + 2 * p), c1[im]);
+        h[s] = hartley_split(Z, Zm);
+      } else {
+        h[s] = make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int k = 2 * p + j;
+      if (k >= n2) break;
+      const double2 z = j ? make_double2(h[0].y, h[1].y) : make_double2(h[0].x, h[1].x);
+      const double2 w = cmulc(z, c2[k]);
+      u[2 * q * n2 + k] = w.x;
+      u[(2 * q + 1) * n2 + k] = w.y;
+    }
+  }
+}
+
+// x2 post (inverse) + scale: v [Fp][n2] -> z [F][n2]
+__global__ void k_bs_post_rows(const double* v, double* z, long F, int n2, const double2* c2, double scale) {
+  const long Q = (F + 1) / 2;
+  GRID_STRIDE(e, (size_t)Q * n2) {
+    const long q = (long)(e / n2);
+    const int k = (int)(e - (size_t)q * n2);
+    const int km = k == 0 ? 0 : n2 - k;
+    const double* r0 = v + 2 * q * n2;
+    const double* r1 = r0 + n2;
+    const double2 Z = cmulc(make_double2(r0[k], r1[k]), c2[k]);
+    const double2 Zm = cmulc(make_double2(r0[km], r1[km]), c2[km]);
+    const double2 h = hartley_split(Z, Zm);
+    z[2 * q * n2 + k] = scale * h.x;
+    if (2 * q + 1 < F) z[(2 * q + 1) * n2 + k] = scale * h.y;
+  }
+}
+
+cudaError_t launch_bs_pre_rows(cudaStream_t st, LaunchCounter* lc, const double* in, double* out, long F, int n2,
+                               const double2* c2) {
+  count(lc);
+  k_bs_pre_rows<<<ew_grid((size_t)((F + 1) / 2) * n2), EW_THREADS, 0, st>>>(in, out, F, n2, c2);
+  return cudaGetLastError();
+}
+cudaError_t launch_bs_rows_to_cols(cudaStream_t st, LaunchCounter* lc, const double* v, double* u, long F, int n1,
+                                   int n2, int P2, const double2* c2, const double2* c1) {
+  count(lc);
+  k_bs_rows_to_cols<<<ew_grid((size_t)((F + 1) / 2) * (P2 / 2)), EW_THREADS, 0, st>>>(v, u, F, n1, n2, P2, c2, c1);
+  return cudaGetLastError();
+}
+cudaError_t launch_bs_cols_filter(cudaStream_t st, LaunchCounter* lc, const double* v, double* u, int nt, int n1,
+                                  int n2, int P2, const double2* c1, const double* lam1, const double* lam2) {
+  count(lc);
+  k_bs_cols_filter<<<ew_grid((size_t)nt * n1 * (P2 / 2)), EW_THREADS, 0, st>>>(v, u, nt, n1, n2, P2, c1, lam1, lam2);
+  return cudaGetLastError();
+}
+cudaError_t launch_bs_cols_to_rows(cudaStream_t st, LaunchCounter* lc, const double* v, double* u, long F, int n1,
+                                   int n2, int P2, const double2* c1, const double2* c2) {
+  count(lc);
+  k_bs_cols_to_rows<<<ew_grid((size_t)((F + 1) / 2) * (P2 / 2)), EW_THREADS, 0, st>>>(v, u, F, n1, n2, P2, c1, c2);
+  return cudaGetLastError();
+}
+cudaError_t launch_bs_post_rows(cudaStream_t st, LaunchCounter* lc, const double* v, double* z, long F, int n2,
+                                const double2* c2, double scale) {
+  count(lc);
+  k_bs_post_rows<<<ew_grid((size_t)((F + 1) / 2) * n2), EW_THREADS, 0, st>>>(v, z, F, n2, c2, scale);
+  return cudaGetLastError();
+}
+
 size_t max_partials_needed(int nt, int n1, int n2) {
   // Row/column/Hartley grids use >= 2*4 fibres per CTA; elementwise grids are
   // capped at 148*8 CTAs.

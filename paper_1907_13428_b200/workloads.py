@@ -70,3 +70,28 @@ def make_problem(name: str, shape=None, ctx=None, seed: int = 1, ybar=None):
     drv = AdmmDriver(op, pc, c["gamma"], cfg, y_lo=c["y"][0], y_hi=c["y"][1], u_lo=c["u"][0],
                      u_hi=c["u"][1], ybar=yb)
     return c, op, pc, drv
+
+
+# BASELINE C1 operator microbenchmark: A = I (x) T_x + T_y (x) I on every
+# slice, T_x = Riesz(1.3) on x2, T_y = Riesz(1.7) on x1, h = 1/(n + 1); no psi,
+# no time term.  Mapped onto the ConstraintOperator with
+# psi = -1 and a zero time factor: out = -psi (L1 + L2) x = (T_y + T_x) x.
+C1 = dict(shape=(256, 1023, 1023), ax=1.3, ay=1.7)
+
+
+def c1_factors(shape=None):
+    from .api import build_riesz
+    nt, n1, n2 = tuple(shape) if shape is not None else C1["shape"]
+    tx = build_riesz(C1["ax"], n2, 1.0 / (n2 + 1))
+    ty = build_riesz(C1["ay"], n1, 1.0 / (n1 + 1))
+    time = (np.zeros(nt), np.zeros(nt))
+    return (nt, n1, n2), time, ty, tx
+
+
+def make_c1(shape=None, ctx=None):
+    """C1 operator and its 2-level spatial T. Chan preconditioner."""
+    from .api import ConstraintOperator, assemble_spatial_precond
+    shp, time, ty, tx = c1_factors(shape)
+    op = ConstraintOperator(time, ty, tx, -1.0, ctx=ctx)
+    return op, assemble_spatial_precond(op)
+
