@@ -83,11 +83,15 @@ struct CCfg {
   static constexpr bool HOMO = FDG_C_HOMO != 0;          // rows
   static constexpr bool HOMO_COL = FDG_C_HOMO_COL != 0;  // columns
   // sub-lane barriers assume T <= 32; the half-row swizzle a power-of-two G
-  static constexpr bool OK = T <= 32 && R >= 2 && (R & 1) == 0 && (G & (G - 1)) == 0;
+  // sub-lanes of T > 32 synchronize with named barriers (fdg_fft.cuh lane_sync)
+  static constexpr bool OK = T <= 64 && R >= 2 && (R & 1) == 0 && (G & (G - 1)) == 0 && G2 <= 8;
+  // twist table in shared memory up to M = 512 (else read through L1, which
+  // leaves room for four staged tiles at L = 2048)
+  static constexpr bool TWS = M <= 512;
   // exchange | M-point twiddles | twist W_L^j (j < M) | symbol (L, real or
   // complex) | staging
   static constexpr size_t bytes(size_t stage_doubles, bool sr) {
-    return sizeof(double2) * (EXB + 2 * (size_t)M) + (sr ? sizeof(double) : sizeof(double2)) * (size_t)L +
+    return sizeof(double2) * (EXB + (TWS ? 2 : 1) * (size_t)M) + (sr ? sizeof(double) : sizeof(double2)) * (size_t)L +
            sizeof(double) * stage_doubles;
   }
 };
@@ -124,9 +128,13 @@ struct CSmem {
     load_table(t, gtw, C::M);
     tw = t;
     t += C::M;
-    load_table(t, gtwist, C::M);
-    twist = t;
-    t += C::M;
+    if constexpr (C::TWS) {
+      load_table(t, gtwist, C::M);
+      twist = t;
+      t += C::M;
+    } else {
+      twist = gtwist;
+    }
     if constexpr (SR) {
       double* d = reinterpret_cast<double*>(t);
       for (int i = threadIdx.x; i < L; i += blockDim.x) d[i] = __ldg(&gsym_re[i]);

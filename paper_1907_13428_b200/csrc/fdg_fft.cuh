@@ -228,7 +228,7 @@ __device__ __forceinline__ void lane_sync(int g) {
 #define FDG_R256 16
 #endif
 #ifndef FDG_R512
-#define FDG_R512 8
+#define FDG_R512 16
 #endif
 __host__ __device__ constexpr int fft_radix(int N) {
   return N <= 8 ? N : (N == 256 ? FDG_R256 : (N == 512 ? FDG_R512 : (N < 512 ? 8 : 16)));

@@ -239,10 +239,13 @@ static inline unsigned clamp_grid(long tiles, int cap) {
 #ifndef FDG_SPLIT_CONV
 #define FDG_SPLIT_CONV 1
 #endif
+#ifndef FDG_SPLIT_LMAX
+#define FDG_SPLIT_LMAX 2048
+#endif
 // Embedding lengths served by the split-spectrum passes (fdg_conv.cuh).
 template <int L>
 struct UseSplit {
-  static constexpr bool value = FDG_SPLIT_CONV && L == 512;
+  static constexpr bool value = FDG_SPLIT_CONV && L >= 512 && L <= FDG_SPLIT_LMAX;
 };
 
 template <int L, int MODE, bool PF, bool SR>
@@ -256,10 +259,6 @@ static cudaError_t run_rowc_s(cudaStream_t st, const RowArgs& a) {
   return pdl_launch(k_rowc<L, MODE, PF, SR>, clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st,
                     a);
 }
-template <int L, int MODE, bool PF>
-static cudaError_t run_rowc_v(cudaStream_t st, const RowArgs& a) {
-  return a.sym_re ? run_rowc_s<L, MODE, PF, true>(st, a) : run_rowc_s<L, MODE, PF, false>(st, a);
-}
 
 template <int L, int MODE, bool PF, bool SR>
 static cudaError_t run_colc_s(cudaStream_t st, const ColArgs& a) {
@@ -271,16 +270,12 @@ static cudaError_t run_colc_s(cudaStream_t st, const ColArgs& a) {
   const long tiles = (long)a.O * ((a.C + 2 * Cf::G - 1) / (2 * Cf::G));
   return pdl_launch(k_colc<L, MODE, PF, SR>, clamp_grid(tiles, cap), Cf::THREADS, SM, st, a);
 }
-template <int L, int MODE, bool PF>
-static cudaError_t run_colc_v(cudaStream_t st, const ColArgs& a) {
-  return a.sym_re ? run_colc_s<L, MODE, PF, true>(st, a) : run_colc_s<L, MODE, PF, false>(st, a);
-}
 
+constexpr size_t kMaxSmem = 227 * 1024;
+
+// direct 2n-point passes (fdg_passes.cuh)
 template <int L, int MODE, bool PF>
-static cudaError_t run_row_v(cudaStream_t st, const RowArgs& a) {
-  if constexpr (UseSplit<L>::value) {
-    return run_rowc_v<L, MODE, PF>(st, a);
-  }
+static cudaError_t run_row_direct(cudaStream_t st, const RowArgs& a) {
   using Cf = Cfg<L>;
   constexpr size_t SM = RowPlan<L, MODE, PF>::SMEM;
   int cap = 0;
@@ -289,15 +284,31 @@ static cudaError_t run_row_v(cudaStream_t st, const RowArgs& a) {
   const long F = (long)a.nt * a.n1;
   return pdl_launch(k_row<L, MODE, PF>, clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st, a);
 }
+template <int L, int MODE, bool PF>
+static cudaError_t run_row_v(cudaStream_t st, const RowArgs& a) {
+  return run_row_direct<L, MODE, PF>(st, a);
+}
 
 template <int L, int MODE>
 static cudaError_t run_row(cudaStream_t st, const RowArgs& a) {
   // pipelined full tiles: n == L/2 and tiles of 2G fibres inside one slice
-  constexpr int G = UseSplit<L>::value ? CCfg<L>::G : Cfg<L>::G;
-  if constexpr (Cfg<L>::PF_OK) {
-    if (2 * a.n == L && a.n1 % (2 * G) == 0) return run_row_v<L, MODE, true>(st, a);
+  if constexpr (UseSplit<L>::value) {
+    // split passes for full staged tiles; ragged shapes take the direct
+    // 2n-point kernels (their unstaged epilogue hides latency better)
+    if (2 * a.n == L && a.n1 % (2 * CCfg<L>::G) == 0) {
+      if (a.sym_re) {
+        if constexpr (RowCPlan<L, MODE, true, true>::SMEM <= kMaxSmem) return run_rowc_s<L, MODE, true, true>(st, a);
+      } else {
+        if constexpr (RowCPlan<L, MODE, true, false>::SMEM <= kMaxSmem) return run_rowc_s<L, MODE, true, false>(st, a);
+      }
+    }
+    return run_row_direct<L, MODE, false>(st, a);
+  } else {
+    if constexpr (Cfg<L>::PF_OK) {
+      if (2 * a.n == L && a.n1 % (2 * Cfg<L>::G) == 0) return run_row_v<L, MODE, true>(st, a);
+    }
+    return run_row_v<L, MODE, false>(st, a);
   }
-  return run_row_v<L, MODE, false>(st, a);
 }
 
 template <int MODE>
@@ -312,10 +323,7 @@ static cudaError_t dispatch_row(cudaStream_t st, int L, const RowArgs& a) {
 }
 
 template <int L, int MODE, bool PF>
-static cudaError_t run_col_v(cudaStream_t st, const ColArgs& a) {
-  if constexpr (UseSplit<L>::value) {
-    return run_colc_v<L, MODE, PF>(st, a);
-  }
+static cudaError_t run_col_direct(cudaStream_t st, const ColArgs& a) {
   using Cf = Cfg<L>;
   constexpr size_t SM = ColPlan<L, PF>::SMEM;
   int cap = 0;
@@ -324,14 +332,28 @@ static cudaError_t run_col_v(cudaStream_t st, const ColArgs& a) {
   const long tiles = (long)a.O * ((a.C + 2 * Cf::G - 1) / (2 * Cf::G));
   return pdl_launch(k_col<L, MODE, PF>, clamp_grid(tiles, cap), Cf::THREADS, SM, st, a);
 }
+template <int L, int MODE, bool PF>
+static cudaError_t run_col_v(cudaStream_t st, const ColArgs& a) {
+  return run_col_direct<L, MODE, PF>(st, a);
+}
 
 template <int L, int MODE>
 static cudaError_t run_col(cudaStream_t st, const ColArgs& a) {
-  constexpr int G = UseSplit<L>::value ? CCfg<L>::G : Cfg<L>::G;
-  if constexpr (Cfg<L>::PF_OK) {
-    if (2 * a.n == L && a.C % (2 * G) == 0) return run_col_v<L, MODE, true>(st, a);
+  if constexpr (UseSplit<L>::value) {
+    if (2 * a.n == L && a.C % (2 * CCfg<L>::G) == 0) {
+      if (a.sym_re) {
+        if constexpr (ColCPlan<L, MODE, true, true>::SMEM <= kMaxSmem) return run_colc_s<L, MODE, true, true>(st, a);
+      } else {
+        if constexpr (ColCPlan<L, MODE, true, false>::SMEM <= kMaxSmem) return run_colc_s<L, MODE, true, false>(st, a);
+      }
+    }
+    return run_col_direct<L, MODE, false>(st, a);
+  } else {
+    if constexpr (Cfg<L>::PF_OK) {
+      if (2 * a.n == L && a.C % (2 * Cfg<L>::G) == 0) return run_col_v<L, MODE, true>(st, a);
+    }
+    return run_col_v<L, MODE, false>(st, a);
   }
-  return run_col_v<L, MODE, false>(st, a);
 }
 
 template <int MODE>

@@ -40,13 +40,13 @@ namespace fdg {
 #define FDG_T256_DB 0
 #endif
 #ifndef FDG_T512_THREADS
-#define FDG_T512_THREADS 256
+#define FDG_T512_THREADS 128
 #endif
 #ifndef FDG_T512_MINB
-#define FDG_T512_MINB 2
+#define FDG_T512_MINB 3
 #endif
 #ifndef FDG_T512_DB
-#define FDG_T512_DB 1
+#define FDG_T512_DB 0
 #endif
 template <int L>
 struct Cfg {
