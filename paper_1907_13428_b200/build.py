@@ -15,13 +15,12 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib", "libfdg.so")
-SOURCES = ["fdg_kernels.cu", "fdg_api.cu"]
-HEADERS = ["fdg_fft.cuh", "fdg_passes.cuh", "fdg_conv.cuh", "fdg_reduce.cuh", "fdg_internal.h"]
+SOURCES = ["fdg_kernels.cu", "fdg_api.cu"] + sorted(
+    f for f in os.listdir(CSRC) if f.startswith("fdg_inst_") and f.endswith(".cu"))
+HEADERS = [f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = [
-    "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-    "-Xcompiler", "-fPIC", "-shared", "--diag-suppress", "177",
-]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "--diag-suppress", "177"]
 
 
 def _stale() -> bool:
@@ -33,18 +32,38 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
-    tmp = LIB + ".tmp"
-    cmd = [NVCC, *FLAGS, "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile every translation unit in parallel (nvcc -c), link libfdg.so."""
+    from concurrent.futures import ThreadPoolExecutor
+    lib = out or LIB
+    if out is None and not defines and not force and not _stale():
+        return lib
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    objdir = os.path.join(os.path.dirname(lib), "obj" + ("" if out is None else "_" + os.path.basename(lib)))
+    os.makedirs(objdir, exist_ok=True)
+    extra = [f"-D{d}" for d in defines]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [NVCC, *FLAGS, *extra, "-c", "-o", obj, os.path.join(CSRC, src)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    tmp = lib + ".tmp"
+    subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs], check=True)
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    args = [a for a in sys.argv[1:] if a != "--force"]
+    # python build.py [--force] [NAME -DDEF ...]: a variant library lib/libfdg_NAME.so
+    if args:
+        name, defs = args[0], [a[2:] for a in args[1:] if a.startswith("-D")]
+        print(build(defines=defs, out=os.path.join(PKG, "lib", f"libfdg_{name}.so"), verbose=False))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

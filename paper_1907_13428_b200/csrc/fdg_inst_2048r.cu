@@ -1,0 +1,9 @@
+// fdg_inst_2048r.cu — explicit instantiation unit (Row passes, embedding length 2048) of the pass launchers in
+// fdg_launch.cuh; one translation unit per group so nvcc compiles them in
+// parallel.
+#define FDG_LAUNCH_DEFS
+#include "fdg_launch.cuh"
+
+namespace fdg {
+FDG_INST_ROW(2048)
+}  // namespace fdg
