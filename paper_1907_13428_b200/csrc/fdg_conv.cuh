@@ -84,7 +84,7 @@ struct CCfg {
   static constexpr bool HOMO_COL = FDG_C_HOMO_COL != 0;  // columns
   // sub-lane barriers assume T <= 32; the half-row swizzle a power-of-two G
   // sub-lanes of T > 32 synchronize with named barriers (fdg_fft.cuh lane_sync)
-  static constexpr bool OK = T <= 64 && R >= 2 && (R & 1) == 0 && (G & (G - 1)) == 0 && G2 <= 8;
+  static constexpr bool OK = T <= 64 && R >= 2 && (R & 1) == 0 && (G & (G - 1)) == 0 && (T <= 32 || G2 <= 8);
   // twist table in shared memory up to M = 512 (else read through L1, which
   // leaves room for four staged tiles at L = 2048)
   static constexpr bool TWS = M <= 512;

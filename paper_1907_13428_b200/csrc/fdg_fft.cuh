@@ -246,6 +246,10 @@ struct PassRadix {
 // (one 128-byte bank window) instead of a power-of-two stride.
 // Host builder: fdg_api.cu stockham_twiddles().
 
+#ifndef FDG_TW_ALL
+#define FDG_TW_ALL 0  // 1: load every twiddle instead of forming products of powers of two
+#endif
+
 // One Stockham pass on a lane (registers in, registers out, with the
 // shared-memory scatter of the pass output unless it is the last pass).
 //   N   : transform length, R: registers per thread, T = N/R
@@ -271,7 +275,7 @@ struct Stockham {
         double2 wt[Rp];
 #pragma unroll
         for (int r = 1; r < Rp; ++r) {
-          if ((r & (r - 1)) == 0) {
+          if (FDG_TW_ALL || (r & (r - 1)) == 0) {
             wt[r] = tw[(r - 1) * Ns];
           } else {
             const int lo = r & -r;
