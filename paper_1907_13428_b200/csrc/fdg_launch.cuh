@@ -178,9 +178,12 @@ cudaError_t run_col_v(cudaStream_t st, const ColArgs& a) {
   return run_col_direct<L, MODE, PF>(st, a);
 }
 
+#ifndef FDG_SPLIT_COL_LMAX
+#define FDG_SPLIT_COL_LMAX 1024  // L = 2048 column tiles (W = 4) lose to the direct kernel
+#endif
 template <int L, int MODE>
 cudaError_t run_col(cudaStream_t st, const ColArgs& a) {
-  if constexpr (UseSplit<L>::value) {
+  if constexpr (UseSplit<L>::value && L <= FDG_SPLIT_COL_LMAX) {
     if (2 * a.n == L && a.C % (2 * CCfg<L>::G) == 0) {
       if (a.sym_re) {
         if constexpr (ColCPlan<L, MODE, true, true>::SMEM <= kMaxSmem) return run_colc_s<L, MODE, true, true>(st, a);
@@ -212,8 +215,11 @@ cudaError_t run_hrow_v(cudaStream_t st, const double* in, double* out, int F, co
 template <int N>
 cudaError_t run_hrow(cudaStream_t st, const double* in, double* out, int F, const double2* tw,
                             const double* rdot, RedSlot red, const int* guard) {
-  if constexpr (Cfg<N>::PF_OK) {
-    if (F % (2 * Cfg<N>::G) == 0) return run_hrow_v<N, true>(st, in, out, F, tw, rdot, red, guard);
+  // staged full tiles; at N = 1024 only for the r.z pass, whose unstaged
+  // epilogue reads of r stall (measured: 1130 -> 652 us at 128 x 1024^2)
+  if constexpr (Cfg<N>::PF_OK || N == 1024) {
+    if (F % (2 * Cfg<N>::G) == 0 && (Cfg<N>::PF_OK || rdot))
+      return run_hrow_v<N, true>(st, in, out, F, tw, rdot, red, guard);
   }
   return run_hrow_v<N, false>(st, in, out, F, tw, rdot, red, guard);
 }

@@ -48,6 +48,9 @@ namespace fdg {
 #ifndef FDG_T512_DB
 #define FDG_T512_DB 0
 #endif
+#ifndef FDG_PF_MAX
+#define FDG_PF_MAX 512  // largest length with staged (cp.async) full-tile variants
+#endif
 template <int L>
 struct Cfg {
   static constexpr int R = fft_radix(L);
@@ -59,7 +62,7 @@ struct Cfg {
   static constexpr bool DB = L == 256 ? (FDG_T256_DB != 0) : (L == 512 ? (FDG_T512_DB != 0) : L <= 512);
   static constexpr bool TS = L <= 1024;
   static constexpr size_t EXB = (size_t)L * G;  // double2 per exchange buffer
-  static constexpr bool PF_OK = L >= 16 && L <= 512;
+  static constexpr bool PF_OK = L >= 16 && L <= FDG_PF_MAX;
 };
 
 // Shared-memory plan: exchange buffer(s) | twiddles | extra table | staging.
