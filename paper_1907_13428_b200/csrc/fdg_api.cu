@@ -611,13 +611,21 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
     auto slot_prv = [](int it) { return (it & 1) ? S_RZ1 : S_RZ0; };
     auto dir_cur = [&](int it) { return (it & 1) ? a->d.d() : a->d2.d(); };
     auto dir_prv = [&](int it) { return (it & 1) ? a->d2.d() : a->d.d(); };
-    // iteration body: S d, r -= a S d, x += a d, control, z = M r (r.z -> next slot)
+    // iteration body: p = z + b p (+ the previous iteration's x += a p, in
+    // K1F), S p, r -= a S p, control, z = M r (r.z -> next slot).  x_host:
+    // last iteration whose x update the host applied itself (after a pause).
+    int x_host = 0;
+    auto x_update = [&](int it) {  // x += (r.z / p^T S p) p of iteration it
+      ck(fdg::launch_axpy_dev(st, lc, x, dir_cur(it), N, sc.at(slot_cur(it)), sc.at(S_PQ)), "x += a p");
+      x_host = it;
+    };
     auto enqueue = [&](int it, bool guarded) {
       const int* g = guarded ? pause : nullptr;
       const int cur = slot_cur(it), prv = slot_prv(it);
-      ck(fdg::launch_row_fused(st, lc, a->z.d(), dir_prv(it), dir_cur(it), nullptr, a->u.d(), op->nt, op->n1,
-                               op->n2, op->row_axis(), op->scale2(), tf, op->psi, nullptr, nullptr, sc.at(cur),
-                               sc.at(prv), it == 1, false, g),
+      const bool upd = it > 1 && x_host != it - 1;  // alpha_{it-1} = rz(prv) / pq (S_PQ still holds pq_{it-1})
+      ck(fdg::launch_row_fused(st, lc, a->z.d(), dir_prv(it), dir_cur(it), x, a->u.d(), op->nt, op->n1, op->n2,
+                               op->row_axis(), op->scale2(), tf, op->psi, sc.at(prv), sc.at(S_PQ), sc.at(cur),
+                               sc.at(prv), it == 1, upd, g),
          "K1F row");
       ck(fdg::launch_col_s_mid(st, lc, dir_cur(it), a->u.d(), a->w.d(), a->vp.d(), op->nt, op->n1, op->n2, op->ax1,
                                op->scale1(), a->inv_m2.d(), a->a1.d(), sc.slot(S_PQ), g),
@@ -625,7 +633,6 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
       ck(fdg::launch_row_s_out(st, lc, a->w.d(), a->vp.d(), nullptr, a->r.d(), op->nt, op->n1, op->n2,
                                op->row_axis(), op->scale2(), tf, op->psi, sc.at(cur), sc.at(S_PQ), sc.slot(S_RR), g),
          "K3 row");
-      ck(fdg::launch_axpy_dev(st, lc, x, dir_cur(it), N, sc.at(cur), sc.at(S_PQ), g), "x += a p");
       double* out = dstat + 4 * (it & 1);
       ck(fdg::launch_pcg_control(st, lc, sc.at(S_PQ), sc.at(S_RR), (tol * nb) * (tol * nb), out, pause, g),
          "control");
@@ -649,7 +656,9 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
           fail(FDG_ENUMERIC, "pcg: operator lost positive definiteness", FDG_NUM_PD_LOSS);
         if (!std::isfinite(rn)) fail(FDG_ENUMERIC, "pcg: non-finite residual", FDG_NUM_NONFINITE_RESIDUAL);
         if (rn <= tol * nb) {
-          // confirm with the true residual (admm.cpp:152-158)
+          // x += a p of iteration it (its carrier, K1F of it+1, was skipped),
+          // then confirm with the true residual (admm.cpp:152-158)
+          x_update(it);
           apply_S_dev(a, x, a->z.d());
           ck(fdg::launch_residual(st, lc, a->r.d(), rhs, a->z.d(), N, sc.slot(S_RR2)), "r = b - Ax");
           double rr2;
@@ -666,6 +675,7 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
         if (it < max_inner) enqueue(it + 1, true);
       }
     }
+    if (max_inner >= 1 && x_host != max_inner) x_update(max_inner);  // no K1F carries the last update
     ck(cudaStreamSynchronize(st), "drain");
   } else {
     int cur = S_RZ0, nxt = S_RZ1;
@@ -1405,9 +1415,9 @@ fdg_status fdg_admm_profile_passes(fdg_admm a, int reps, double* ms, double* byt
     std::vector<std::function<void()>> passes = {
         [&] {
           if (op->tf.kind != 2)
-            ck(fdg::launch_row_fused(st, lc, a->z.d(), a->d2.d(), a->d.d(), nullptr, a->u.d(), op->nt, op->n1,
-                                     op->n2, op->row_axis(), op->scale2(), stf, op->psi, nullptr, nullptr,
-                                     sc.at(S_RZ0), sc.at(S_RZ1), false, false),
+            ck(fdg::launch_row_fused(st, lc, a->z.d(), a->d2.d(), a->d.d(), a->tmp.d(), a->u.d(), op->nt, op->n1,
+                                     op->n2, op->row_axis(), op->scale2(), stf, op->psi, sc.at(S_RZ1), sc.at(S_PQ),
+                                     sc.at(S_RZ0), sc.at(S_RZ1), false, true),
                "K1F");
           else
             ck(fdg::launch_row_apply(st, lc, a->d.d(), a->u.d(), op->nt, op->n1, op->n2, op->row_axis(),
@@ -1430,8 +1440,10 @@ fdg_status fdg_admm_profile_passes(fdg_admm a, int reps, double* ms, double* byt
     };
     // algorithmic HBM bytes per launch (each N-vector read or written once)
     const double nb = 8.0 * (double)N;
-    // K1F: reads z, d_old; writes d_new, u.  X: x += a p (3N).
-    const double k1 = op->tf.kind != 2 ? 4 * nb : 2 * nb;
+    // K1F: reads z, d_old, x; writes d_new, u, x (the x update of the
+    // previous iteration rides along).  X: the stand-alone x += a p, run once
+    // per solve (the last iteration's update), not per iteration.
+    const double k1 = op->tf.kind != 2 ? 6 * nb : 2 * nb;
     const double alg[9] = {k1, 4 * nb, 4 * nb, 2 * nb, 2 * nb, 2 * nb, 2 * nb, 3 * nb, 3 * nb};
     for (size_t i = 0; i < passes.size(); ++i) {
       passes[i]();  // warm

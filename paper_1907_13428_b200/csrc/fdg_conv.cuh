@@ -312,10 +312,25 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
   const double* in1 = a.dold;
   const ptrdiff_t noff = (ptrdiff_t)a.tdir * a.n1 * n;
   double acc = 0.0;
+  // MODE 2 full tiles: the previous iteration's x += alpha d_old rides here
+  // (d_old is staged anyway); x of the owned positions is prefetched into
+  // registers one tile ahead so its latency hides behind a whole tile.
+  constexpr bool XPF = MODE == 2 && PF;
+  double2 xpre[XPF ? HR : 1];
+  const bool upd_x = XPF && a.upd_x && !first;
+  auto load_x = [&](int tl) {
+    const size_t rx = (size_t)(tl * 2 * G + 2 * g) * n;
+#pragma unroll
+    for (int i = 0; i < (XPF ? HR : 1); ++i) {
+      const int pos = t + T * (i + b * HR);
+      xpre[i] = make_double2(a.xs[rx + pos], a.xs[rx + n + pos]);
+    }
+  };
   if constexpr (PF) {
     if (blockIdx.x < ntiles) {
       FDG_IO(stage_rows(st_in, in0 + (size_t)blockIdx.x * 2 * G * n, TILE));
       if (MODE == 2 && !first) FDG_IO(stage_rows(st_in2, in1 + (size_t)blockIdx.x * 2 * G * n, TILE));
+      if (upd_x) load_x(blockIdx.x);
     }
     cp_async_commit();
   }
@@ -335,16 +350,28 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
         const int pos = t + m * T;
         double2 z = make_double2(st_in[(2 * g) * M + pos], st_in[(2 * g + 1) * M + pos]);
         if constexpr (MODE == 2) {
+          double2 dd = make_double2(0.0, 0.0);
           if (!first) {
-            z.x += beta * st_in2[(2 * g) * M + pos];
-            z.y += beta * st_in2[(2 * g + 1) * M + pos];
+            dd = make_double2(st_in2[(2 * g) * M + pos], st_in2[(2 * g + 1) * M + pos]);
+            z.x += beta * dd.x;
+            z.y += beta * dd.y;
           }
           if ((m < HR) == (b == 0)) {
             FDG_IO(a.dnew[ra + pos] = z.x);
             FDG_IO(a.dnew[ra + n + pos] = z.y);
+            if constexpr (XPF) {
+              if (upd_x) {
+                const int i = m < HR ? m : m - HR;  // static: only the owning half stores
+                FDG_IO(a.xs[ra + pos] = xpre[i].x + alpha * dd.x);
+                FDG_IO(a.xs[ra + n + pos] = xpre[i].y + alpha * dd.y);
+              }
+            }
           }
         }
         v[m] = z;
+      }
+      if constexpr (XPF) {
+        if (upd_x && tile + (int)gridDim.x < ntiles) load_x(tile + gridDim.x);
       }
       __syncthreads();  // st_in and the epilogue staging are free
       const int k = f0 / a.n1;
@@ -424,7 +451,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
         }
         if constexpr (MODE == 0 || MODE == 2) {
           FDG_IO(a.out[o] = val);
-          if (MODE == 2 && a.upd_x) FDG_IO(a.xs[o] += alpha * __ldg(in1 + o));
+          if (MODE == 2 && !XPF && a.upd_x && !first) FDG_IO(a.xs[o] += alpha * __ldg(in1 + o));
         } else {
           const double q = (SEPI ? st_vp[sl] : __ldg(&a.vp[o])) + val;
           if (a.q_out) a.q_out[o] = q;
