@@ -288,6 +288,7 @@ enum Scal {
   S_DINF = S_ADMM + 4,  // 2
   S_OBJ = S_DINF + 2,   // 2
   S_DOT = S_OBJ + 2,
+  S_ONE,  // constant 1.0 (alpha of the fused residual r = b - 1 * S x)
   S_COUNT
 };
 
@@ -301,6 +302,8 @@ struct Scalars {
     counters.alloc(sizeof(unsigned) * S_COUNT);
     ck(cudaMemset(vals.p, 0, sizeof(double) * S_COUNT), "memset");
     ck(cudaMemset(counters.p, 0, sizeof(unsigned) * S_COUNT), "memset");
+    const double one = 1.0;
+    ck(cudaMemcpy(vals.d() + S_ONE, &one, sizeof(double), cudaMemcpyHostToDevice), "H2D");
   }
   double* at(int s) const { return vals.d() + s; }
   RedSlot slot(int s) const {
@@ -503,7 +506,11 @@ fdg::AdmmScalars admm_scalars(const fdg_admm_s* a) {
 
 // q = S x (admm.cpp:87-98), fused: row(x) -> u; col(x,u) -> w, vp (+pq);
 // row(w, vp) -> q.  pq lands in S_PQ.
-void apply_S_dev(fdg_admm_s* a, const double* x, double* q) {
+// r_out != null: instead of q, r_out = b - S x (the reference's residual,
+// admm.cpp:133-136 / 152-154) with |r_out|^2 reduced into red -- fused into
+// the last pass as r_out = b - 1 * q.
+void apply_S_dev(fdg_admm_s* a, const double* x, double* q, double* r_out = nullptr, const double* b = nullptr,
+                 RedSlot red = RedSlot{}) {
   fdg_op_s* op = a->op;
   cudaStream_t st = op->ctx->stream;
   LaunchCounter* lc = &op->ctx->lc;
@@ -523,9 +530,15 @@ void apply_S_dev(fdg_admm_s* a, const double* x, double* q) {
     ck(fdg::launch_col_acc(st, lc, a->w.d(), a->vp.d(), a->vp.d(), 1, op->nt, op->n1 * op->n2, tf.fft,
                            op->psi / tf.fft.L, true),
        "S t adj");
-  ck(fdg::launch_row_s_out(st, lc, a->w.d(), a->vp.d(), q, nullptr, op->nt, op->n1, op->n2, op->row_axis(), op->scale2(),
-                           tf.kind == 1 ? tf : none_tf, op->psi, nullptr, nullptr, RedSlot{}),
-     "S row adj");
+  if (r_out)
+    ck(fdg::launch_row_s_out(st, lc, a->w.d(), a->vp.d(), q, r_out, op->nt, op->n1, op->n2, op->row_axis(),
+                             op->scale2(), tf.kind == 1 ? tf : none_tf, op->psi, a->sc.at(S_ONE), a->sc.at(S_ONE), red,
+                             nullptr, b),
+       "S row adj + residual");
+  else
+    ck(fdg::launch_row_s_out(st, lc, a->w.d(), a->vp.d(), q, nullptr, op->nt, op->n1, op->n2, op->row_axis(),
+                             op->scale2(), tf.kind == 1 ? tf : none_tf, op->psi, nullptr, nullptr, RedSlot{}),
+       "S row adj");
 }
 
 // Search-direction product fused with the residual update:
@@ -583,13 +596,16 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
     finish();
     return res;
   }
+  // x = 0: r = b; the fused schedule reads b in place of r until the first
+  // residual update (no copy)
+  const bool fused = a->op->tf.kind != 2;
+  const bool r_is_b = std::sqrt(h[1]) == 0.0 && fused;
   if (std::sqrt(h[1]) == 0.0) {
-    ck(fdg::launch_copy(st, lc, a->r.d(), rhs, N), "r = b");
+    if (!fused) ck(fdg::launch_copy(st, lc, a->r.d(), rhs, N), "r = b");
   } else {
-    apply_S_dev(a, x, a->z.d());
-    ck(fdg::launch_residual(st, lc, a->r.d(), rhs, a->z.d(), N, sc.slot(S_RR2)), "r = b - Ax");
+    apply_S_dev(a, x, nullptr, a->r.d(), rhs, sc.slot(S_RR2));
   }
-  if (a->op->tf.kind != 2) {
+  if (fused) {
     // Fused schedule: the CG update x += a p; p = z + b p of
     // iteration k-1 (p = z + b p) runs inside the B row pass of iteration k
     // (K1F), with ping-pong direction buffers (neighbour time slices of the
@@ -631,7 +647,8 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
                                op->scale1(), a->inv_m2.d(), a->a1.d(), sc.slot(S_PQ), g),
          "K2 col");
       ck(fdg::launch_row_s_out(st, lc, a->w.d(), a->vp.d(), nullptr, a->r.d(), op->nt, op->n1, op->n2,
-                               op->row_axis(), op->scale2(), tf, op->psi, sc.at(cur), sc.at(S_PQ), sc.slot(S_RR), g),
+                               op->row_axis(), op->scale2(), tf, op->psi, sc.at(cur), sc.at(S_PQ), sc.slot(S_RR), g,
+                               it == 1 && r_is_b ? rhs : nullptr),
          "K3 row");
       double* out = dstat + 4 * (it & 1);
       ck(fdg::launch_pcg_control(st, lc, sc.at(S_PQ), sc.at(S_RR), (tol * nb) * (tol * nb), out, pause, g),
@@ -640,7 +657,8 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
       ck(cudaEventRecord(a->ev_stat[it & 1], st), "event");
       pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(prv), pause);  // r.z' -> prv slot
     };
-    pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(slot_cur(1)));
+    const double* r0 = r_is_b ? rhs : a->r.d();
+    pc_apply_dev(a->pc, r0, a->z.d(), a->u.d(), r0, sc.slot(slot_cur(1)));
     if (max_inner >= 1) enqueue(1, true);
     for (int it = 1; it <= max_inner; ++it) {
       if (it < max_inner) enqueue(it + 1, true);  // speculative
@@ -659,8 +677,7 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
           // x += a p of iteration it (its carrier, K1F of it+1, was skipped),
           // then confirm with the true residual (admm.cpp:152-158)
           x_update(it);
-          apply_S_dev(a, x, a->z.d());
-          ck(fdg::launch_residual(st, lc, a->r.d(), rhs, a->z.d(), N, sc.slot(S_RR2)), "r = b - Ax");
+          apply_S_dev(a, x, nullptr, a->r.d(), rhs, sc.slot(S_RR2));
           double rr2;
           sc.read(S_RR2, 1, &rr2);
           rn = std::sqrt(rr2);
@@ -695,8 +712,7 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
         // confirm with the true residual (admm.cpp:152-158)
         ck(fdg::launch_axpy_dev(st, lc, x, a->d.d(), N, sc.at(cur), sc.at(S_PQ)), "x += a p");
         x_done = true;
-        apply_S_dev(a, x, a->z.d());
-        ck(fdg::launch_residual(st, lc, a->r.d(), rhs, a->z.d(), N, sc.slot(S_RR2)), "r = b - Ax");
+        apply_S_dev(a, x, nullptr, a->r.d(), rhs, sc.slot(S_RR2));
         double rr2;
         sc.read(S_RR2, 1, &rr2);
         rn = std::sqrt(rr2);
@@ -715,8 +731,7 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
     }
   }
   // cap: true relative residual (admm.cpp:165-168)
-  apply_S_dev(a, x, a->z.d());
-  ck(fdg::launch_residual(st, lc, a->u.d(), rhs, a->z.d(), N, sc.slot(S_RR2)), "res");
+  apply_S_dev(a, x, nullptr, a->u.d(), rhs, sc.slot(S_RR2));
   double rr2;
   sc.read(S_RR2, 1, &rr2);
   res = {max_inner, 0, std::sqrt(rr2) / nb, 0.0};

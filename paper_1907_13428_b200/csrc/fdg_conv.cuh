@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
         }
         if constexpr (MODE == 1) {
           FDG_IO(stage_rows(st_vp, a.vp + (size_t)f0 * n, TILE));
-          if (a.r) FDG_IO(stage_rows(st_r, a.r + (size_t)f0 * n, TILE));
+          if (a.r) FDG_IO(stage_rows(st_r, (a.r_in ? a.r_in : a.r) + (size_t)f0 * n, TILE));
         }
       }
       cp_async_commit();  // group E
@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
           const double q = (SEPI ? st_vp[sl] : __ldg(&a.vp[o])) + val;
           if (a.q_out) a.q_out[o] = q;
           if (a.r) {
-            const double rn = (SEPI ? st_r[sl] : a.r[o]) - alpha * q;
+            const double rn = (SEPI ? st_r[sl] : (a.r_in ? a.r_in : a.r)[o]) - alpha * q;
             FDG_IO(a.r[o] = rn);
             acc += rn * rn;
           }

@@ -79,7 +79,8 @@ cudaError_t launch_col_s_mid(cudaStream_t st, LaunchCounter* lc, const double* p
 cudaError_t launch_row_s_out(cudaStream_t st, LaunchCounter* lc, const double* w, const double* vp,
                              double* q_out, double* r, int nt, int n1, int n2, const AxisSym& s2,
                              double scale, const TimeFactor& tf, double psi, const double* alpha_num,
-                             const double* alpha_den, RedSlot red, const int* guard = nullptr);
+                             const double* alpha_den, RedSlot red, const int* guard = nullptr,
+                             const double* r_in = nullptr);
 
 // Fused CG update + B row pass (K9 folded into K1): d_new = z + beta d_old
 // (beta = *b_num / *b_den; first: d_new = z), written to dnew and used as the

@@ -228,9 +228,10 @@ cudaError_t launch_row_apply(cudaStream_t st, LaunchCounter* lc, const double* x
 cudaError_t launch_row_s_out(cudaStream_t st, LaunchCounter* lc, const double* w, const double* vp, double* q_out,
                              double* r, int nt, int n1, int n2, const AxisSym& s2, double scale,
                              const TimeFactor& tf, double psi, const double* alpha_num, const double* alpha_den,
-                             RedSlot red, const int* guard) {
+                             RedSlot red, const int* guard, const double* r_in) {
   RowArgs a{};
   a.guard = guard;
+  a.r_in = r_in;
   a.x = w;
   a.vp = vp;
   a.q_out = q_out;

@@ -136,6 +136,7 @@ struct RowArgs {
   double* out;
   double* q_out;
   double* r;
+  const double* r_in;  // MODE 1: r = r_in - alpha q (null: r_in = r)
   int nt, n1, n;
   const double2* sym;
   const double2* tw;
@@ -269,7 +270,7 @@ __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_row(RowArgs a
       }
       if constexpr (MODE == 1) {
         stage_rows(st_vp, a.vp + (size_t)f0 * n, TILE);
-        if (a.r) stage_rows(st_r, a.r + (size_t)f0 * n, TILE);
+        if (a.r) stage_rows(st_r, (a.r_in ? a.r_in : a.r) + (size_t)f0 * n, TILE);
       }
       cp_async_commit();  // group E: this tile's epilogue operands
       const int nxt = tile + gridDim.x;
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_row(RowArgs a
           const double q = (PF ? st_vp[sl] : __ldg(&a.vp[o])) + val;
           if (a.q_out) a.q_out[o] = q;
           if (a.r) {
-            const double rn = (PF ? st_r[sl] : a.r[o]) - alpha * q;
+            const double rn = (PF ? st_r[sl] : (a.r_in ? a.r_in : a.r)[o]) - alpha * q;
             a.r[o] = rn;
             acc += rn * rn;
           }
