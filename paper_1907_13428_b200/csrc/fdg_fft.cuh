@@ -211,9 +211,18 @@ struct Ex {
 // private region, so only the lane's T threads synchronize: __syncwarp when a
 // lane is (part of) one warp, a named barrier (id 1 + lane) otherwise.  Lanes
 // then run their FFTs independently instead of in CTA-wide lock step.
-template <int LAYOUT, int T>
+#ifndef FDG_HALF_BAR
+#define FDG_HALF_BAR 1
+#endif
+// LAYOUT 2 (split-interleaved rows of GW sub-lanes, even half | odd half):
+// the sub-lanes of one half exchange only among themselves, so each half
+// synchronizes its (GW/2) * T threads on a named barrier (id 1 + half)
+// instead of the whole CTA.
+template <int LAYOUT, int T, int GW = 1>
 __device__ __forceinline__ void lane_sync(int g) {
-  if constexpr (LAYOUT == 0 || LAYOUT == 2) {
+  if constexpr (LAYOUT == 2 && FDG_HALF_BAR && GW >= 2) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + (g >= GW / 2)), "n"((GW / 2) * T) : "memory");
+  } else if constexpr (LAYOUT == 0 || LAYOUT == 2) {
     __syncthreads();
   } else if constexpr (T <= 32) {
     __syncwarp();
@@ -294,7 +303,7 @@ struct Stockham {
 #endif
     }
     if constexpr (!LAST) {
-      if (ex.single()) lane_sync<LAYOUT, T>(g);  // write-after-read on the single buffer
+      if (ex.single()) lane_sync<LAYOUT, T, G>(g);  // write-after-read on the single buffer
       double2* sm = ex.next();
       // scatter: out[(b/Ns)*Ns*Rp + b%Ns + r*Ns] = v[s + r*S]
 #ifndef FDG_EXP_NOEX
@@ -306,7 +315,7 @@ struct Stockham {
         for (int r = 0; r < Rp; ++r) sm[slot<LAYOUT, N, G>(base + r * Ns, g)] = v[s + r * S];
       }
 #endif
-      lane_sync<LAYOUT, T>(g);
+      lane_sync<LAYOUT, T, G>(g);
 #ifndef FDG_EXP_NOEX
 #pragma unroll
       for (int m = 0; m < R; ++m) v[m] = sm[slot<LAYOUT, N, G>(t + m * T, g)];
@@ -332,11 +341,11 @@ __device__ __forceinline__ void fft_lane(double2 (&v)[R], Ex& ex, int t, int g, 
 template <int N, int R, int G, int LAYOUT = 0>
 __device__ __forceinline__ void mirror_lane(const double2 (&v)[R], double2 (&w)[R], Ex& ex, int t, int g) {
   constexpr int T = N / R;
-  if (ex.single()) lane_sync<LAYOUT, T>(g);
+  if (ex.single()) lane_sync<LAYOUT, T, G>(g);
   double2* sm = ex.next();
 #pragma unroll
   for (int m = 0; m < R; ++m) sm[slot<LAYOUT, N, G>(t + m * T, g)] = v[m];
-  lane_sync<LAYOUT, T>(g);
+  lane_sync<LAYOUT, T, G>(g);
 #pragma unroll
   for (int m = 0; m < R; ++m) {
     const int pos = t + m * T;
@@ -358,11 +367,11 @@ __device__ __forceinline__ double2 hartley_split(double2 z, double2 w) {
 template <int N, int R, int G, int LAYOUT = 0>
 __device__ __forceinline__ void hartley_lane(double2 (&v)[R], Ex& ex, int t, int g) {
   constexpr int T = N / R;
-  if (ex.single()) lane_sync<LAYOUT, T>(g);
+  if (ex.single()) lane_sync<LAYOUT, T, G>(g);
   double2* sm = ex.next();
 #pragma unroll
   for (int m = 0; m < R; ++m) sm[slot<LAYOUT, N, G>(t + m * T, g)] = v[m];
-  lane_sync<LAYOUT, T>(g);
+  lane_sync<LAYOUT, T, G>(g);
 #pragma unroll
   for (int m = 0; m < R; ++m) {
     const int mp = (N - (t + m * T)) & (N - 1);
