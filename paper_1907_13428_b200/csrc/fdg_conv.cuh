@@ -189,10 +189,15 @@ struct CMap {
 };
 
 // Barrier over the two sub-lanes of every lane.
+// Lane-major HOMO rows with T <= 32: lane g's halves are warps
+// (g T / 32) and (G T / 32 + g T / 32); the two warps meet on named barrier
+// 1 + g T / 32 (the sub-lane exchanges use __syncwarp, no ids).
 template <int L, int LAYOUT, bool HOMO>
-__device__ __forceinline__ void pair_sync() {
+__device__ __forceinline__ void pair_sync(int g = 0) {
   using C = CCfg<L>;
-  if constexpr (LAYOUT != 1 || HOMO || C::LT > 32) {
+  if constexpr (LAYOUT == 1 && HOMO && C::T <= 32 && (C::G * C::T) % 32 == 0 && FDG_HALF_BAR) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(1 + (g * C::T) / 32), "n"(64) : "memory");
+  } else if constexpr (LAYOUT != 1 || HOMO || C::LT > 32) {
     __syncthreads();
   } else {
     __syncwarp();
@@ -245,20 +250,20 @@ __device__ __forceinline__ void conv_combine(const double2 (&v)[CCfg<L>::R], dou
   for (int i = 0; i < HR; ++i) y[i] = b ? v[i + HR] : v[i];
   return;
 #endif
-  pair_sync<L, LAYOUT, HM>();  // write-after-read: last inverse-FFT exchange
+  pair_sync<L, LAYOUT, HM>(mp.g);  // write-after-read: last inverse-FFT exchange
   double2* sm = ex.next();
 #pragma unroll
   for (int i = 0; i < HR; ++i) {
     const double2 val = b ? v[i] : v[i + HR];
     sm[slot<LAYOUT, M, G2>(t + T * (b ? i : i + HR), mp.gs)] = val;
   }
-  pair_sync<L, LAYOUT, HM>();
+  pair_sync<L, LAYOUT, HM>(mp.g);
 #pragma unroll
   for (int i = 0; i < HR; ++i) {
     const double2 mine = b ? v[i + HR] : v[i];
     y[i] = cadd(mine, sm[slot<LAYOUT, M, G2>(t + T * (i + b * HR), mp.partner)]);
   }
-  if constexpr (TRAIL) pair_sync<L, LAYOUT, HM>();
+  if constexpr (TRAIL) pair_sync<L, LAYOUT, HM>(mp.g);
 }
 
 // =================================================================== rows
