@@ -286,7 +286,7 @@ def run_b200(args):
     peak, peak_kind = _peaks()
     passes = drv.profile_passes(args.profile_reps)
     for p in passes.values():
-        p["gbs"] = p["bytes"] / (p["ms"] * 1e-3) / 1e9
+        p["gbs"] = p["bytes"] / (p["ms"] * 1e-3) / 1e9 if p["ms"] > 0 else None  # 0: fused into a neighbour
     dom_name = max(passes, key=lambda k: passes[k]["ms"])
     dom = passes[dom_name]
     traffic = None

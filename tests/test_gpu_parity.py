@@ -118,7 +118,11 @@ def test_precond_golden(gpu_ctx, golden, n):
     assert rel(pc.solve(golden[f"ie{n}_x"]), golden[f"ie{n}_Minv_x"]) < OP_TOL
 
 
-@pytest.mark.parametrize("shape", [(4, 8, 16), (16, 8, 4), (32, 64, 64), (8, 128, 32), (1, 32, 64)])
+@pytest.mark.parametrize("shape", [(4, 8, 16), (16, 8, 4), (32, 64, 64), (8, 128, 32), (1, 32, 64),
+                                   # n1 == n2 in {256, 512}: x2/x1 pairs fused through L2, fewer
+                                   # and more slabs than the pipeline lag
+                                   (1, 256, 256), (4, 256, 256), (32, 256, 256), (2, 512, 512),
+                                   (16, 512, 512)])
 def test_precond_noncube_vs_port(gpu_ctx, port, shape):
     from oracle import implicit_euler
     from paper_1907_13428_b200 import assemble_precond
