@@ -178,6 +178,9 @@ cudaError_t run_col_v(cudaStream_t st, const ColArgs& a) {
   return run_col_direct<L, MODE, PF>(st, a);
 }
 
+#ifndef FDG_PF_COL2048
+#define FDG_PF_COL2048 0  // 1: spills at 128 registers (measured 4.1 vs 3.2 ms at C4)
+#endif
 #ifndef FDG_SPLIT_COL_LMAX
 #define FDG_SPLIT_COL_LMAX 1024  // L = 2048 column tiles (W = 4) lose to the direct kernel
 #endif
@@ -193,7 +196,9 @@ cudaError_t run_col(cudaStream_t st, const ColArgs& a) {
     }
     return run_col_direct<L, MODE, false>(st, a);
   } else {
-    if constexpr (Cfg<L>::PF_OK) {
+    // staged full tiles for the direct column kernel also at L = 2048 (the
+    // unstaged x1 pass of C4 stalls on global loads: long_scoreboard 5.6)
+    if constexpr (Cfg<L>::PF_OK || (L == 2048 && FDG_PF_COL2048)) {
       if (2 * a.n == L && a.C % (2 * Cfg<L>::G) == 0) return run_col_v<L, MODE, true>(st, a);
     }
     return run_col_v<L, MODE, false>(st, a);
