@@ -5,6 +5,7 @@
 // over device-resident state.  Per Krylov iteration only two scalars (p^T S p
 // and |r|^2) cross to the host, for the reference's convergence and
 // breakdown checks (admm.cpp:143-158).
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -504,9 +505,14 @@ struct fdg_admm_s {
   cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr;
   // speculative PCG: device pause flag, per-parity (pq, |r|^2) status, its
   // pinned host mirror and completion events
-  DevBuf ctl, dstat;
+  // status words live in host-mapped pinned memory written by the control
+  // kernel (no copy node in the stream); hseq[parity] = the sequence number
+  // of the latest enqueue of an iteration of that parity
+  DevBuf ctl;
   double* hstat = nullptr;
-  cudaEvent_t ev_stat[2] = {nullptr, nullptr};
+  double* hstat_dev = nullptr;
+  double seq = 0.0;
+  double hseq[2] = {0.0, 0.0};
 };
 
 namespace {
@@ -580,6 +586,23 @@ void s_and_update(fdg_admm_s* a, const double* dd, const double* rz_slot) {
      "K3 row");
 }
 
+// Spin until the control kernel published the status words of sequence
+// number `seq` (host-mapped memory); a failed stream ends the wait.
+void wait_status(cudaStream_t st, const volatile double* hs, double seq) {
+  for (unsigned spin = 0;; ++spin) {
+    if (hs[3] == seq) break;
+    if ((spin & 1023u) == 1023u) {
+      const cudaError_t e = cudaStreamQuery(st);
+      if (e == cudaSuccess) {
+        if (hs[3] == seq) break;
+        fail(FDG_ECUDA, "pcg: control status missing");
+      }
+      if (e != cudaErrorNotReady) ck(e, "status");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+}
+
 // pcg (admm.cpp:121-169) with apply = apply_S, precond = pc.solve.
 fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, int max_inner) {
   fdg_ctx ctx = a->op->ctx;
@@ -632,7 +655,6 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
     fdg_op_s* op = a->op;
     const TimeFactor& tf = op->tf;
     int* pause = static_cast<int*>(a->ctl.p);
-    double* dstat = a->dstat.d();
     ck(cudaMemsetAsync(pause, 0, sizeof(int), st), "clear pause");
     auto slot_cur = [](int it) { return (it & 1) ? S_RZ0 : S_RZ1; };  // r.z used by iteration it
     auto slot_prv = [](int it) { return (it & 1) ? S_RZ1 : S_RZ0; };
@@ -661,11 +683,11 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
                                op->row_axis(), op->scale2(), tf, op->psi, sc.at(cur), sc.at(S_PQ), sc.slot(S_RR), g,
                                it == 1 && r_is_b ? rhs : nullptr),
          "K3 row");
-      double* out = dstat + 4 * (it & 1);
-      ck(fdg::launch_pcg_control(st, lc, sc.at(S_PQ), sc.at(S_RR), (tol * nb) * (tol * nb), out, pause, g),
+      a->seq += 1.0;
+      a->hseq[it & 1] = a->seq;
+      ck(fdg::launch_pcg_control(st, lc, sc.at(S_PQ), sc.at(S_RR), (tol * nb) * (tol * nb),
+                                 a->hstat_dev + 4 * (it & 1), pause, g, a->seq),
          "control");
-      ck(cudaMemcpyAsync(a->hstat + 4 * (it & 1), out, 3 * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
-      ck(cudaEventRecord(a->ev_stat[it & 1], st), "event");
       pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(prv), pause);  // r.z' -> prv slot
     };
     const double* r0 = r_is_b ? rhs : a->r.d();
@@ -673,8 +695,8 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
     if (max_inner >= 1) enqueue(1, true);
     for (int it = 1; it <= max_inner; ++it) {
       if (it < max_inner) enqueue(it + 1, true);  // speculative
-      ck(cudaEventSynchronize(a->ev_stat[it & 1]), "status");
-      const double* hs = a->hstat + 4 * (it & 1);
+      const volatile double* hs = a->hstat + 4 * (it & 1);
+      wait_status(st, hs, a->hseq[it & 1]);
       const double pq = hs[0];
       double rn = std::sqrt(hs[1]);
       if (hs[2] != 0.0) {
@@ -1270,12 +1292,11 @@ fdg_status fdg_admm_create(fdg_op op, fdg_pc pc, const fdg_admm_desc* desc, cons
     a->sc.init(ctx);
     a->inner_tol = d.inner_tol_factor * d.inner_tol_floor;  // admm.cpp:245
     for (cudaEvent_t* e : {&a->e0, &a->e1, &a->e2, &a->e3}) ck(cudaEventCreate(e), "event");
-    for (cudaEvent_t* e : {&a->ev_stat[0], &a->ev_stat[1]})
-      ck(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "event");
     a->ctl.alloc(sizeof(int) * 4);
     ck(cudaMemsetAsync(a->ctl.p, 0, sizeof(int) * 4, st), "memset");
-    a->dstat.alloc(sizeof(double) * 8);
-    ck(cudaMallocHost(&a->hstat, sizeof(double) * 8), "pinned");
+    ck(cudaHostAlloc(&a->hstat, sizeof(double) * 8, cudaHostAllocMapped), "pinned status");
+    for (int i = 0; i < 8; ++i) a->hstat[i] = -1.0;
+    ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a->hstat_dev), a->hstat, 0), "mapped status");
     ck(cudaStreamSynchronize(st), "sync");
     *out = a.release();
   });
@@ -1286,7 +1307,7 @@ fdg_status fdg_admm_destroy(fdg_admm a) {
     if (!a) return;
     a->op->ctx->set_device();
     cudaStreamSynchronize(a->op->ctx->stream);
-    for (cudaEvent_t e : {a->e0, a->e1, a->e2, a->e3, a->ev_stat[0], a->ev_stat[1]})
+    for (cudaEvent_t e : {a->e0, a->e1, a->e2, a->e3})
       if (e) cudaEventDestroy(e);
     if (a->hstat) cudaFreeHost(a->hstat);
     delete a;

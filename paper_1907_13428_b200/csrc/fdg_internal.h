@@ -113,7 +113,7 @@ cudaError_t launch_pc_pipe(cudaStream_t st, LaunchCounter* lc, const double* in,
 // out[1] = |r|^2 (copied for the host); raises *pause when the host must act
 // (pq <= 0 / non-finite, non-finite residual, or |r| <= tol |b|).
 cudaError_t launch_pcg_control(cudaStream_t st, LaunchCounter* lc, const double* pq, const double* rr,
-                               double tol_nb2, double* out, int* pause, const int* guard);
+                               double tol_nb2, double* out, int* pause, const int* guard, double seq);
 
 // ------------------------------------------------------------- elementwise
 cudaError_t launch_copy(cudaStream_t st, LaunchCounter* lc, double* dst, const double* src, size_t N);

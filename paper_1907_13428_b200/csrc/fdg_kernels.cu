@@ -377,7 +377,7 @@ cudaError_t launch_t_filter(cudaStream_t st, LaunchCounter* lc, double* data, co
 // iteration may run: breakdown checks and the reference's true-residual
 // confirmation (admm.cpp:143-158).
 __global__ void k_pcg_control(const double* pq, const double* rr, double tol_nb2, double* out, int* pause,
-                              const int* guard) {
+                              const int* guard, double seq) {
   pdl_trigger();
   pdl_wait();
   if (guard && *reinterpret_cast<const volatile int*>(guard)) return;
@@ -387,16 +387,31 @@ __global__ void k_pcg_control(const double* pq, const double* rr, double tol_nb2
   // exact comparison
   const bool bad = !isfinite(p) || p <= 0.0 || !isfinite(r2);
   const bool stop = bad || r2 <= tol_nb2 * (1.0 + 1e-12);
-  out[0] = p;
-  out[1] = r2;
-  out[2] = stop ? 1.0 : 0.0;
   if (stop) *pause = 1;
+  // out is host-mapped pinned memory: the values, then (after a system
+  // fence) the sequence number the host spins on
+  volatile double* o = out;
+  o[0] = p;
+  o[1] = r2;
+  o[2] = stop ? 1.0 : 0.0;
+  __threadfence_system();
+  o[3] = seq;
 }
 
 cudaError_t launch_pcg_control(cudaStream_t st, LaunchCounter* lc, const double* pq, const double* rr,
-                               double tol_nb2, double* out, int* pause, const int* guard) {
+                               double tol_nb2, double* out, int* pause, const int* guard, double seq) {
   count(lc);
-  return pdl_launch(k_pcg_control, 1, 1, 0, st, pq, rr, tol_nb2, out, pause, guard);
+#if FDG_CARVEOUT
+  static int dev_set = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev_set != dev) {
+    cudaFuncSetAttribute(k_pcg_control, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    dev_set = dev;
+  }
+#endif
+  return pdl_launch(k_pcg_control, 1, 1, 0, st, pq, rr, tol_nb2, out, pause, guard, seq);
 }
 
 cudaError_t launch_copy(cudaStream_t st, LaunchCounter* lc, double* dst, const double* src, size_t N) {

@@ -28,6 +28,9 @@ template <int N>
 cudaError_t run_tf(cudaStream_t st, double* data, const PcTables& pt, const int* guard);
 
 // ================================================================ dispatch
+#ifndef FDG_CARVEOUT
+#define FDG_CARVEOUT 1
+#endif
 #define FDG_POW2_CASES(X) X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048)
 
 // Opt in to > 48 KB dynamic shared memory and size the persistent grid
@@ -44,6 +47,12 @@ inline cudaError_t prep(size_t smem, int threads, int& grid_cap) {
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (ls.device != dev) {
+    // every pass kernel asks for the max-shared L1 split, so consecutive
+    // kernels of the PCG chain never force an SM reconfiguration drain
+#if FDG_CARVEOUT
+    e = cudaFuncSetAttribute(K, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+#endif
     if (smem > 48 * 1024) {
       e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
