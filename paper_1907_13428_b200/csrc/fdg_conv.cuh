@@ -206,11 +206,14 @@ __device__ __forceinline__ void pair_sync(int g = 0) {
 
 // Sub-lane b's half of the convolution, in place on v (input z[t + T m] for
 // every m; output that half's contribution at the same positions).
+// The forward and the inverse transform share their per-thread twiddles
+// (TwCache) when the M-point transform has a single twiddled pass.
 template <int L, int LAYOUT, bool SR>
 __device__ __forceinline__ void conv_half(double2 (&v)[CCfg<L>::R], Ex& ex, int t, int gs, int b,
                                           const double2* tw, const double2* twist, const SymTab<SR>& sym) {
   using C = CCfg<L>;
   constexpr int M = C::M, R = C::R, T = C::T, G2 = C::G2;
+  constexpr bool CACHE = FDG_TWCACHE && TwCache<M, R>::OK;
 #ifdef FDG_EXP_NOCONV
   return;
 #endif
@@ -220,12 +223,13 @@ __device__ __forceinline__ void conv_half(double2 (&v)[CCfg<L>::R], Ex& ex, int 
     for (int m = 0; m < R; ++m) v[m] = cmul(v[m], twist[t + T * m]);
   }
 #endif
-  fft_lane<M, R, G2, false, LAYOUT>(v, ex, t, gs, tw);
+  double2 wc[TwCache<M, R>::K];
+  fft_lane_c<M, R, G2, false, LAYOUT, CACHE ? 1 : 0>(v, ex, t, gs, tw, wc);
 #ifndef FDG_EXP_NOSYM
 #pragma unroll
   for (int m = 0; m < R; ++m) v[m] = sym.apply(v[m], 2 * (t + T * m) + b);
 #endif
-  fft_lane<M, R, G2, true, LAYOUT>(v, ex, t, gs, tw);
+  fft_lane_c<M, R, G2, true, LAYOUT, CACHE ? 2 : 0>(v, ex, t, gs, tw, wc);
 #ifndef FDG_EXP_NOTWIST
   if (b) {
 #pragma unroll

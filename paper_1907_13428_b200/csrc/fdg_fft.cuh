@@ -306,7 +306,21 @@ struct PassRadix {
 //   N   : transform length, R: registers per thread, T = N/R
 //   Ns  : product of previous radices, OFF: offset of this pass in ptw
 //   G   : lanes per CTA (smem row width)
-template <int N, int R, int G, bool INV, int Ns, int LAYOUT, int OFF = 0>
+// Twiddle cache (CM): a transform with ONE twiddled pass (N <= R^2) has
+// per-thread twiddles that depend only on the thread's position in its lane,
+// so a forward / inverse pair (or several transforms of one thread) can form
+// them once: CM = 1 forms and stores them in wc[s*Rp + r], CM = 2 reads wc
+// (inverse passes use the conjugates of the same values).
+#ifndef FDG_TWCACHE
+#define FDG_TWCACHE 1
+#endif
+template <int N, int R>
+struct TwCache {
+  static constexpr bool OK = N > R && N / R <= R;
+  static constexpr int K = OK ? R : 1;  // S * Rp of the twiddled pass
+};
+
+template <int N, int R, int G, bool INV, int Ns, int LAYOUT, int OFF = 0, int CM = 0>
 struct Stockham {
   static constexpr int T = N / R;
   static constexpr int Rp = PassRadix<N, R, Ns>::value;
@@ -315,6 +329,15 @@ struct Stockham {
   static constexpr int NEXT_OFF = OFF + (Ns > 1 ? (Rp - 1) * Ns : 0);
 
   __device__ __forceinline__ static void run(double2 (&v)[R], Ex& ex, int t, int g, const double2* ptw) {
+    double2 wc[1];
+    static_assert(CM == 0, "twiddle cache needs its array");
+    run(v, ex, t, g, ptw, wc);
+  }
+
+  template <int CK>
+  __device__ __forceinline__ static void run(double2 (&v)[R], Ex& ex, int t, int g, const double2* ptw,
+                                             double2 (&wc)[CK]) {
+    static_assert(CM == 0 || (TwCache<N, R>::OK && CK >= TwCache<N, R>::K), "twiddle cache shape");
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int b = t + s * T;  // butterfly index in [0, N/Rp)
@@ -324,13 +347,22 @@ struct Stockham {
         // pipe, not FP64, is the busiest unit of these kernels.
         const double2* tw = ptw + OFF + (b & (Ns - 1));
         double2 wt[Rp];
+        if constexpr (CM == 2) {
 #pragma unroll
-        for (int r = 1; r < Rp; ++r) {
-          if (FDG_TW_ALL || (r & (r - 1)) == 0) {
-            wt[r] = tw[(r - 1) * Ns];
-          } else {
-            const int lo = r & -r;
-            wt[r] = cmul(wt[lo], wt[r - lo]);
+          for (int r = 1; r < Rp; ++r) wt[r] = wc[s * Rp + r];
+        } else {
+#pragma unroll
+          for (int r = 1; r < Rp; ++r) {
+            if (FDG_TW_ALL || (r & (r - 1)) == 0) {
+              wt[r] = tw[(r - 1) * Ns];
+            } else {
+              const int lo = r & -r;
+              wt[r] = cmul(wt[lo], wt[r - lo]);
+            }
+          }
+          if constexpr (CM == 1) {
+#pragma unroll
+            for (int r = 1; r < Rp; ++r) wc[s * Rp + r] = wt[r];
           }
         }
 #ifndef FDG_EXP_NOMATH
@@ -362,7 +394,7 @@ struct Stockham {
 #pragma unroll
       for (int m = 0; m < R; ++m) v[m] = sm[slot<LAYOUT, N, G>(t + m * T, g)];
 #endif
-      Stockham<N, R, G, INV, Ns * Rp, LAYOUT, NEXT_OFF>::run(v, ex, t, g, ptw);
+      Stockham<N, R, G, INV, Ns * Rp, LAYOUT, NEXT_OFF, CM>::run(v, ex, t, g, ptw, wc);
     }
   }
 };
@@ -376,6 +408,13 @@ __device__ __forceinline__ void fft_lane(double2 (&v)[R], Ex& ex, int t, int g, 
   } else {
     Stockham<N, R, G, INV, 1, LAYOUT>::run(v, ex, t, g, tw);
   }
+}
+
+// fft_lane with the twiddle cache (TwCache): CM = 1 fills wc, CM = 2 uses it.
+template <int N, int R, int G, bool INV, int LAYOUT, int CM, int CK>
+__device__ __forceinline__ void fft_lane_c(double2 (&v)[R], Ex& ex, int t, int g, const double2* tw,
+                                           double2 (&wc)[CK]) {
+  Stockham<N, R, G, INV, 1, LAYOUT, 0, CM>::run(v, ex, t, g, tw, wc);
 }
 
 // Exchange helper: value at position (N - pos) mod N for every register

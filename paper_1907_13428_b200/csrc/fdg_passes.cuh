@@ -699,7 +699,13 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(doub
       for (int m = 0; m < R; ++m)
         v[m] = vc ? col_get<false>(data + (size_t)(t + m * T) * C + c, C, c) : make_double2(0.0, 0.0);
     }
-    fft_lane<N, R, G, false>(v, S.ex, t, g, S.tw);
+    // both transforms are forward Hartley transforms of the same length; the
+    // second could reuse the first one's per-thread twiddles (TwCache), but
+    // the cache pushes this kernel over its 168-register bound (measured:
+    // spills, no gain), so it is off here
+    constexpr int TCM = 0;
+    double2 wc[TwCache<N, R>::K];
+    fft_lane_c<N, R, G, false, 0, TCM>(v, S.ex, t, g, S.tw, wc);
     hartley_lane<N, R, G>(v, S.ex, t, g);
     // spatial eigenvalue sums of the two packed columns
     double2 sa = make_double2(0.0, 0.0), sb = make_double2(0.0, 0.0);
@@ -726,7 +732,7 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(doub
       const double inv = pt.inv_total * frcp(lsa * lsb);
       v[m] = make_double2(h.x * (lsb * inv), h.y * (lsa * inv));
     }
-    fft_lane<N, R, G, false>(v, S.ex, t, g, S.tw);
+    fft_lane_c<N, R, G, false, 0, 2 * TCM>(v, S.ex, t, g, S.tw, wc);
     hartley_lane<N, R, G>(v, S.ex, t, g);
 #pragma unroll
     for (int m = 0; m < R; ++m)
