@@ -206,6 +206,9 @@ __device__ __forceinline__ void pair_sync(int g = 0) {
 
 // Sub-lane b's half of the convolution, in place on v (input z[t + T m] for
 // every m; output that half's contribution at the same positions).
+#ifndef FDG_BAL_TWIST
+#define FDG_BAL_TWIST 1
+#endif
 // The forward and the inverse transform share their per-thread twiddles
 // (TwCache) when the M-point transform has a single twiddled pass.
 template <int L, int LAYOUT, bool SR>
@@ -231,7 +234,9 @@ __device__ __forceinline__ void conv_half(double2 (&v)[CCfg<L>::R], Ex& ex, int 
 #endif
   fft_lane_c<M, R, G2, true, LAYOUT, CACHE ? 2 : 0>(v, ex, t, gs, tw, wc);
 #ifndef FDG_EXP_NOTWIST
-  if (b) {
+  // FDG_BAL_TWIST: the odd half's post-twist W_L^-j is applied in
+  // conv_combine, each half twisting the odd values of its own positions
+  if (b && !FDG_BAL_TWIST) {
 #pragma unroll
     for (int m = 0; m < R; ++m) v[m] = cmulc(v[m], twist[t + T * m]);
   }
@@ -242,9 +247,12 @@ __device__ __forceinline__ void conv_half(double2 (&v)[CCfg<L>::R], Ex& ex, int 
 // those for m >= R/2; y[i] is position t + T (i + b R/2).  Each store
 // instruction writes one half-row of both halves (conflict-free).  TRAIL:
 // barrier after the reads (when no other barrier precedes the next scatter).
+// FDG_BAL_TWIST: v of the odd half is not yet post-twisted; the odd half
+// twists its own positions, the even half the odd values it receives (8
+// twist multiplies per thread instead of 16 on the odd half only).
 template <int L, int LAYOUT, bool TRAIL, class Map>
 __device__ __forceinline__ void conv_combine(const double2 (&v)[CCfg<L>::R], double2 (&y)[CCfg<L>::HR], Ex& ex,
-                                             const Map& mp) {
+                                             const Map& mp, const double2* twist) {
   constexpr bool HM = Map::HOMO;
   using C = CCfg<L>;
   constexpr int M = C::M, T = C::T, G2 = C::G2, HR = C::HR;
@@ -264,8 +272,15 @@ __device__ __forceinline__ void conv_combine(const double2 (&v)[CCfg<L>::R], dou
   pair_sync<L, LAYOUT, HM>(mp.g);
 #pragma unroll
   for (int i = 0; i < HR; ++i) {
-    const double2 mine = b ? v[i + HR] : v[i];
-    y[i] = cadd(mine, sm[slot<LAYOUT, M, G2>(t + T * (i + b * HR), mp.partner)]);
+    const int pos = t + T * (i + b * HR);
+    double2 mine = b ? v[i + HR] : v[i];
+    double2 other = sm[slot<LAYOUT, M, G2>(pos, mp.partner)];
+#if FDG_BAL_TWIST && !defined(FDG_EXP_NOTWIST)
+    const double2 w = twist[pos];
+    if (b) mine = cmulc(mine, w);
+    else other = cmulc(other, w);
+#endif
+    y[i] = cadd(mine, other);
   }
   if constexpr (TRAIL) pair_sync<L, LAYOUT, HM>(mp.g);
 }
@@ -426,7 +441,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
     }
     conv_half<L, 1>(v, S.ex, t, mp.gs, b, S.tw, S.twist, S.sym);
     double2 y[HR];
-    conv_combine<L, 1, !PF>(v, y, S.ex, mp);
+    conv_combine<L, 1, !PF>(v, y, S.ex, mp, S.twist);
 
     if constexpr (SEPI) {
       cp_async_wait<1>();
@@ -564,7 +579,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
     }
     conv_half<L, LY>(v, S.ex, t, mp.gs, b, S.tw, S.twist, S.sym);
     double2 y[HR];
-    conv_combine<L, LY, !PF && MODE == 0>(v, y, S.ex, mp);
+    conv_combine<L, LY, !PF && MODE == 0>(v, y, S.ex, mp, S.twist);
 
     if constexpr (MODE == 0) {
 #pragma unroll
@@ -609,7 +624,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
 #pragma unroll
       for (int m = 0; m < R; ++m) v[m] = sm[slot<LY, M, G2>(t + T * m, m < HR ? id0 : id1)];
       conv_half<L, LY>(v, S.ex, t, mp.gs, b, S.tw, S.twist, S.sym);
-      conv_combine<L, LY, !PF>(v, y, S.ex, mp);
+      conv_combine<L, LY, !PF>(v, y, S.ex, mp, S.twist);
 #pragma unroll
       for (int i = 0; i < HR; ++i) {
         const int pos = t + T * (i + b * HR);
