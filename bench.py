@@ -304,6 +304,24 @@ def run_b200(args):
                  "bytes": B_IT_VECTORS * 8.0 * N, "ms_per_iteration": it_ms,
                  "achieved_gbs": B_IT_VECTORS * 8.0 * N / (it_ms * 1e-3) / 1e9}
     iter_roof["frac"] = iter_roof["achieved_gbs"] / peak
+    # steady-state Krylov iteration: the marginal device time of one more
+    # iteration inside a solve (solves capped at k_lo and k_hi iterations with
+    # an unreachable tolerance; slope of the medians), i.e. the iteration's
+    # cost without the per-solve preconditioner start / true-residual check
+    k_lo, k_hi = 4, 12
+    t_cap = {}
+    for _ in range(3):
+        for k in (k_lo, k_hi):
+            x.zero_()
+            torch.cuda.current_stream().synchronize()
+            t_cap.setdefault(k, []).append(drv.pcg_dev(rhs, x, 1e-300, k).ms)
+    slope_ms = (statistics.median(t_cap[k_hi]) - statistics.median(t_cap[k_lo])) / (k_hi - k_lo)
+    steady = {"method": f"slope of PCG solve time between {k_lo} and {k_hi} capped iterations "
+                        "(median of 3, CUDA events on the library stream)",
+              "ms_per_iteration": slope_ms,
+              "achieved_gbs": B_IT_VECTORS * 8.0 * N / (slope_ms * 1e-3) / 1e9,
+              "fixed_ms_per_solve": statistics.median(t_cap[k_lo]) - k_lo * slope_ms}
+    steady["frac"] = steady["achieved_gbs"] / peak
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -326,7 +344,8 @@ def run_b200(args):
                 "config": _config(shape, {"iters_per_step": iters / args.steps,
                                           "pcg_ms_inside_api": pcg_ms / args.steps}),
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roofline,
-                "iteration_roofline": iter_roof, "passes": passes, "admm": admm,
+                "iteration_roofline": iter_roof, "steady_state_iteration": steady,
+                "passes": passes, "admm": admm,
                 "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     if dist:
@@ -337,7 +356,7 @@ def run_b200(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--shape", type=int, nargs=3, default=[256, 256, 256])
