@@ -14,6 +14,7 @@
 #include <complex>
 #include <cstdio>
 #include <cstring>
+#include <exception>
 #include <functional>
 #include <memory>
 #include <random>
@@ -511,6 +512,12 @@ struct fdg_admm_s {
   DevBuf ctl;
   double* hstat = nullptr;
   double* hstat_dev = nullptr;
+  // host-buffer solve (fdg_admm_pcg_host): copy stream, x0 landing buffer and
+  // its nonzero flag (allocated on first use)
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_x0 = nullptr;
+  DevBuf x0buf, x0flag;
+  int* x0flag_host = nullptr;  // pinned
   double seq = 0.0;
   double hseq[2] = {0.0, 0.0};
 };
@@ -604,7 +611,11 @@ void wait_status(cudaStream_t st, const volatile double* hs, double seq) {
 }
 
 // pcg (admm.cpp:121-169) with apply = apply_S, precond = pc.solve.
-fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, int max_inner) {
+// on_final_x (optional): called right after the x update that precedes a
+// true-residual confirmation is enqueued (x then holds the candidate result;
+// the host-buffer path starts its D2H there, overlapping the confirmation).
+fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, int max_inner,
+                       const std::function<void()>& on_final_x = nullptr) {
   fdg_ctx ctx = a->op->ctx;
   cudaStream_t st = ctx->stream;
   LaunchCounter* lc = &ctx->lc;
@@ -710,6 +721,7 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
           // x += a p of iteration it (its carrier, K1F of it+1, was skipped),
           // then confirm with the true residual (admm.cpp:152-158)
           x_update(it);
+          if (on_final_x) on_final_x();
           apply_S_dev(a, x, nullptr, a->r.d(), rhs, sc.slot(S_RR2));
           double rr2;
           sc.read(S_RR2, 1, &rr2);
@@ -1307,8 +1319,10 @@ fdg_status fdg_admm_destroy(fdg_admm a) {
     if (!a) return;
     a->op->ctx->set_device();
     cudaStreamSynchronize(a->op->ctx->stream);
-    for (cudaEvent_t e : {a->e0, a->e1, a->e2, a->e3})
+    for (cudaEvent_t e : {a->e0, a->e1, a->e2, a->e3, a->ev_x0})
       if (e) cudaEventDestroy(e);
+    if (a->cstream) cudaStreamDestroy(a->cstream);
+    if (a->x0flag_host) cudaFreeHost(a->x0flag_host);
     if (a->hstat) cudaFreeHost(a->hstat);
     delete a;
   });
@@ -1402,10 +1416,62 @@ fdg_status fdg_admm_pcg_host(fdg_admm a, const double* rhs, double* x, double to
     a->op->ctx->set_device();
     cudaStream_t st = a->op->ctx->stream;
     const size_t bytes = sizeof(double) * a->N;
+    // Speculation on the common x0 = 0 start (admm.cpp:131 branch r = b):
+    // the solve starts as soon as rhs has landed, from a zeroed device x,
+    // while x0 travels on a copy stream into its own buffer and is checked
+    // for nonzeros there.  x0 == 0 (every element +-0): the speculative solve
+    // is exactly the reference's (0 + v == v), its x is the result.  Else the
+    // solve is redone from the landed x0.  x is in/out: the D2H of the result
+    // is ordered after the H2D of x0 on the copy stream.
+    if (!a->cstream) {
+      ck(cudaStreamCreateWithFlags(&a->cstream, cudaStreamNonBlocking), "copy stream");
+      ck(cudaEventCreateWithFlags(&a->ev_x0, cudaEventDisableTiming), "event");
+      a->x0buf.alloc(bytes);
+      a->x0flag.alloc(sizeof(int));
+      ck(cudaMallocHost(&a->x0flag_host, sizeof(int)), "pinned flag");
+    }
+    cudaStream_t cs = a->cstream;
+    LaunchCounter* lc = &a->op->ctx->lc;
+    int* flag = static_cast<int*>(a->x0flag.p);
     ck(cudaMemcpyAsync(a->rhs.p, rhs, bytes, cudaMemcpyHostToDevice, st), "H2D rhs");
-    ck(cudaMemcpyAsync(a->tmp.p, x, bytes, cudaMemcpyHostToDevice, st), "H2D x");
-    const fdg_pcg_result r = pcg_dev(a, a->rhs.d(), a->tmp.d(), tol, max_inner);
-    ck(cudaMemcpyAsync(x, a->tmp.p, bytes, cudaMemcpyDeviceToHost, st), "D2H x");
+    ck(cudaMemsetAsync(a->tmp.p, 0, bytes, st), "x = 0");
+    ck(cudaEventRecord(a->ev_x0, st), "event");  // x0's H2D queues behind rhs's
+    ck(cudaStreamWaitEvent(cs, a->ev_x0, 0), "wait");
+    ck(cudaMemsetAsync(flag, 0, sizeof(int), cs), "flag");
+    ck(cudaMemcpyAsync(a->x0buf.p, x, bytes, cudaMemcpyHostToDevice, cs), "H2D x0");
+    ck(fdg::launch_any_nonzero(cs, lc, a->x0buf.d(), a->N, flag), "x0 check");
+    volatile int* hflag = a->x0flag_host;
+    *hflag = -1;
+    ck(cudaMemcpyAsync(a->x0flag_host, flag, sizeof(int), cudaMemcpyDeviceToHost, cs), "flag D2H");
+    // D2H of a candidate x on the copy stream while the confirmation runs
+    // (only once the x0 = 0 speculation is known to hold)
+    bool copied = false;
+    auto early_d2h = [&]() {
+      copied = false;
+      if (cudaStreamQuery(cs) != cudaSuccess || *hflag != 0) return;
+      ck(cudaEventRecord(a->ev_x0, st), "event");
+      ck(cudaStreamWaitEvent(cs, a->ev_x0, 0), "wait");
+      ck(cudaMemcpyAsync(x, a->tmp.p, bytes, cudaMemcpyDeviceToHost, cs), "D2H x (early)");
+      copied = true;
+    };
+    fdg_pcg_result r{};
+    std::exception_ptr spec_error;
+    try {
+      r = pcg_dev(a, a->rhs.d(), a->tmp.d(), tol, max_inner, early_d2h);
+    } catch (...) {
+      spec_error = std::current_exception();  // only binding when x0 == 0
+      cudaStreamSynchronize(st);
+    }
+    ck(cudaStreamSynchronize(cs), "copy stream");
+    const int nz = *hflag;
+    if (!nz && spec_error) std::rethrow_exception(spec_error);
+    if (nz) {
+      r = pcg_dev(a, a->rhs.d(), a->x0buf.d(), tol, max_inner);
+      ck(cudaMemcpyAsync(x, a->x0buf.p, bytes, cudaMemcpyDeviceToHost, st), "D2H x");
+    } else if (!(copied && r.converged)) {
+      // the early copy (if any) predates a failed confirmation or the cap
+      ck(cudaMemcpyAsync(x, a->tmp.p, bytes, cudaMemcpyDeviceToHost, st), "D2H x");
+    }
     ck(cudaStreamSynchronize(st), "sync");
     if (res) *res = r;
   });

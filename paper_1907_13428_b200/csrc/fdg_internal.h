@@ -118,6 +118,8 @@ cudaError_t launch_pcg_control(cudaStream_t st, LaunchCounter* lc, const double*
 // ------------------------------------------------------------- elementwise
 cudaError_t launch_copy(cudaStream_t st, LaunchCounter* lc, double* dst, const double* src, size_t N);
 cudaError_t launch_fill(cudaStream_t st, LaunchCounter* lc, double* dst, double v, size_t N);
+// *flag = 1 when some element of x is not zero (flag is not cleared)
+cudaError_t launch_any_nonzero(cudaStream_t st, LaunchCounter* lc, const double* x, size_t N, int* flag);
 // sum of squares (or dot when b != null) -> red.result[0]
 cudaError_t launch_dot(cudaStream_t st, LaunchCounter* lc, const double* a, const double* b, size_t N,
                        RedSlot red);

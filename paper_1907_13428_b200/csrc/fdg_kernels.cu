@@ -42,6 +42,13 @@ __global__ void k_copy(double* dst, const double* src, size_t N) {
 __global__ void k_fill(double* dst, double v, size_t N) {
   GRID_STRIDE(i, N) dst[i] = v;
 }
+// *flag = 1 if some x[i] is not +-0 (NaN included): norm2(x) != 0 without a
+// reduction (admm.cpp:131), for the host-buffer solve's x0 check.
+__global__ void k_any_nonzero(const double* x, size_t N, int* flag) {
+  bool nz = false;
+  GRID_STRIDE(i, N) nz |= !(x[i] == 0.0);
+  if (__syncthreads_or(nz) && threadIdx.x == 0) *flag = 1;
+}
 __global__ void k_dot(const double* a, const double* b, size_t N, RedSlot red) {
   __shared__ double scratch[32];
   double s = 0.0;
@@ -422,6 +429,11 @@ cudaError_t launch_copy(cudaStream_t st, LaunchCounter* lc, double* dst, const d
 cudaError_t launch_fill(cudaStream_t st, LaunchCounter* lc, double* dst, double v, size_t N) {
   count(lc);
   k_fill<<<ew_grid(N), EW_THREADS, 0, st>>>(dst, v, N);
+  return cudaGetLastError();
+}
+cudaError_t launch_any_nonzero(cudaStream_t st, LaunchCounter* lc, const double* x, size_t N, int* flag) {
+  count(lc);
+  k_any_nonzero<<<ew_grid(N), EW_THREADS, 0, st>>>(x, N, flag);
   return cudaGetLastError();
 }
 cudaError_t launch_dot(cudaStream_t st, LaunchCounter* lc, const double* a, const double* b, size_t N,

@@ -234,3 +234,31 @@ def test_pcg_noncube_vs_port(gpu_ctx, port, shape):
     for _ in range(2):
         g, cpu = drv.step(), padm.step()
         assert abs(g.inner_iters - cpu["inner_iters"]) <= 1
+
+
+@pytest.mark.parametrize("x0_kind", ["zero", "negzero", "warm", "one_nonzero"])
+def test_pcg_host_x0_paths(gpu_ctx, ref, golden, x0_kind):
+    """fdg_admm_pcg_host speculates on x0 = 0 while x0 is in flight and redoes
+    the solve from x0 otherwise: its result must equal the device-buffer path
+    (fdg_admm_pcg) from the same x0 bit for bit, with the same count."""
+    import torch
+    n = 8
+    _, drv = _drivers(gpu_ctx, ref, n, golden[f"ie{n}_ybar"])
+    rhs, _ = drv.build_rhs()
+    N = rhs.size
+    x0 = np.zeros(N)
+    if x0_kind == "negzero":
+        x0[:] = -0.0
+    elif x0_kind == "warm":
+        x0 = golden[f"ie{n}_pcg0_y"] * 0.9
+    elif x0_kind == "one_nonzero":
+        x0[N - 1] = 1e-3
+    xh = x0.copy()
+    _, r_host = drv.pcg(rhs, xh, tol=1e-8, max_inner=400)
+    rhs_d = torch.tensor(rhs, dtype=torch.float64, device="cuda")
+    x_d = torch.tensor(x0, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    r_dev = drv.pcg_dev(rhs_d, x_d, 1e-8, 400)
+    torch.cuda.synchronize()
+    assert r_host.iterations == r_dev.iterations
+    assert np.array_equal(xh, x_d.cpu().numpy())
