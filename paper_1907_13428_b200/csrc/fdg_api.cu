@@ -330,6 +330,7 @@ struct fdg_op_s {
   std::vector<double> tcol, trow, c1, r1, c2, r2;
   DevBuf sym1, tw1, sym2, tw2, symt, symt_adj, twt, sym2s;
   DevBuf twh1, twh2, twht, tws1, tws2, twst;  // split passes: L/2-point twiddles, W_L^j (j < L/2)
+  DevBuf twq1a, twq1b, twq2a, twq2b, twqta, twqtb;  // Q-split passes: 256-point plan, W_L
   DevBuf symr1, symr2, symrt, symr2s;          // real symbols of symmetric factors
   AxisSym ax1, ax2;
   AxisSym ax2s;  // x2 axis with the stencil diagonal folded in: sym2 - c0 (row passes)
@@ -357,7 +358,8 @@ std::vector<double> real_parts(const std::vector<double>& c) {
 }
 
 void build_axis(fdg_op_s* op, AxisSym& ax, DevBuf& sym, DevBuf* sym_adj, DevBuf& tw, DevBuf& twh, DevBuf& tws,
-                DevBuf& symr, const std::vector<double>& col, const std::vector<double>& row) {
+                DevBuf& symr, const std::vector<double>& col, const std::vector<double>& row, DevBuf& twq256,
+                DevBuf& twqf) {
   const int n = (int)col.size();
   const int L = std::max(2, pow2_ceil(2L * n - 1));
   if (L > 2048) fail(FDG_EUNSUPPORTED, "fdg: factor size " + std::to_string(n) + " exceeds the compiled kernel set (n <= 1024)");
@@ -385,6 +387,13 @@ void build_axis(fdg_op_s* op, AxisSym& ax, DevBuf& sym, DevBuf* sym_adj, DevBuf&
   upload(tws, twist, op->ctx->stream);
   ax.twh = twh.c();
   ax.twist = tws.c();
+  if (L >= 1024) {
+    // Q-split passes (fdg_convq.cuh): 256-point plan and the full W_L table
+    upload(twq256, stockham_twiddles(256), op->ctx->stream);
+    upload(twqf, twiddles(L), op->ctx->stream);
+    ax.tw256 = twq256.c();
+    ax.twq = twqf.c();
+  }
   ax.sym_adj = ax.sym;
   if (sym_adj && !symmetric) {
     upload(*sym_adj, embed_symbol_full(row, col, L), op->ctx->stream);
@@ -949,8 +958,10 @@ fdg_status fdg_op_create(fdg_ctx ctx, int nt, int n1, int n2, const double* tcol
     // As in the reference, the adjoint transposes only the time factor; the
     // spatial passes use the forward symbols in both directions
     // (toeplitz.cpp:178-181, "Riesz factors are symmetric").
-    build_axis(op.get(), op->ax1, op->sym1, nullptr, op->tw1, op->twh1, op->tws1, op->symr1, op->c1, op->r1);
-    build_axis(op.get(), op->ax2, op->sym2, nullptr, op->tw2, op->twh2, op->tws2, op->symr2, op->c2, op->r2);
+    build_axis(op.get(), op->ax1, op->sym1, nullptr, op->tw1, op->twh1, op->tws1, op->symr1, op->c1, op->r1, op->twq1a,
+               op->twq1b);
+    build_axis(op.get(), op->ax2, op->sym2, nullptr, op->tw2, op->twh2, op->tws2, op->symr2, op->c2, op->r2, op->twq2a,
+               op->twq2b);
     bool bidiag = true;
     for (int k = 1; k < nt; ++k)
       if (op->trow[k] != 0.0) bidiag = false;
@@ -976,7 +987,8 @@ fdg_status fdg_op_create(fdg_ctx ctx, int nt, int n1, int n2, const double* tcol
       }
     } else {
       op->tf.kind = 2;
-      build_axis(op.get(), op->tf.fft, op->symt, &op->symt_adj, op->twt, op->twht, op->twst, op->symrt, op->tcol, op->trow);
+      build_axis(op.get(), op->tf.fft, op->symt, &op->symt_adj, op->twt, op->twht, op->twst, op->symrt, op->tcol, op->trow,
+                 op->twqta, op->twqtb);
       op->ax2s = op->ax2;
     }
     ctx->ensure_partials(fdg::max_partials_needed(nt, n1, n2));

@@ -24,6 +24,8 @@ struct AxisSym {
   const double2* twist = nullptr;    // W_L^j, j < L/2 (split passes, fdg_conv.cuh)
   const double* sym_re = nullptr;      // real copy of sym when the factor is symmetric
   const double* sym_adj_re = nullptr;  // real copy of sym_adj
+  const double2* tw256 = nullptr;      // Q-split passes (L >= 1024): 256-point plan
+  const double2* twq = nullptr;        // Q-split passes: W_L^k, k < L
 };
 
 // Time coupling.  kind 0: no time term; 1: lower-bidiagonal stencil

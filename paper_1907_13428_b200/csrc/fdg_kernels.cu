@@ -223,6 +223,8 @@ cudaError_t launch_row_apply(cudaStream_t st, LaunchCounter* lc, const double* x
   a.tw = s2.tw;
   a.twh = s2.twh;
   a.twist = s2.twist;
+  a.tw256 = s2.tw256;
+  a.twq = s2.twq;
   a.scale = scale;
   a.tkind = tf.kind == 1 ? 1 : 0;
   a.tc0 = 0.0;  // folded into the x2 symbol (fdg_api.cu ax2s)
@@ -251,6 +253,8 @@ cudaError_t launch_row_s_out(cudaStream_t st, LaunchCounter* lc, const double* w
   a.tw = s2.tw;
   a.twh = s2.twh;
   a.twist = s2.twist;
+  a.tw256 = s2.tw256;
+  a.twq = s2.twq;
   a.scale = scale;
   a.tkind = tf.kind == 1 ? 1 : 0;
   a.tc0 = 0.0;  // folded into the x2 symbol (fdg_api.cu ax2s)
@@ -283,6 +287,8 @@ cudaError_t launch_row_fused(cudaStream_t st, LaunchCounter* lc, const double* z
   a.tw = s2.tw;
   a.twh = s2.twh;
   a.twist = s2.twist;
+  a.tw256 = s2.tw256;
+  a.twq = s2.twq;
   a.scale = scale;
   a.tkind = tf.kind == 1 ? 1 : 0;
   a.tc0 = 0.0;
@@ -312,6 +318,8 @@ cudaError_t launch_col_acc(cudaStream_t st, LaunchCounter* lc, const double* x, 
   a.tw = s.tw;
   a.twh = s.twh;
   a.twist = s.twist;
+  a.tw256 = s.tw256;
+  a.twq = s.twq;
   a.scale = scale;
   count(lc);
   return dispatch_col<0>(st, s.L, a);
@@ -334,6 +342,8 @@ cudaError_t launch_col_s_mid(cudaStream_t st, LaunchCounter* lc, const double* p
   a.tw = s1.tw;
   a.twh = s1.twh;
   a.twist = s1.twist;
+  a.tw256 = s1.tw256;
+  a.twq = s1.twq;
   a.scale = scale;
   a.inv_m2 = inv_m2;
   a.a1 = a1;

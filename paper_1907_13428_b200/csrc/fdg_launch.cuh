@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include "fdg_conv.cuh"
+#include "fdg_convq.cuh"
 #include "fdg_fft.cuh"
 #include "fdg_internal.h"
 #include "fdg_passes.cuh"
@@ -150,8 +151,40 @@ cudaError_t run_row_v(cudaStream_t st, const RowArgs& a) {
   return run_row_direct<L, MODE, PF>(st, a);
 }
 
+#ifndef FDG_QSPLIT
+#define FDG_QSPLIT 1
+#endif
+// Q-split passes (fdg_convq.cuh) for full tiles with real symbols.  Rows at
+// L = 1024 only: measured at 128 x 512^2 K3 383 -> 369 us, K1 equal; at
+// L = 2048 (Q = 8) the input/output combinations and the scattered twist
+// loads cost more than the shorter transforms save (K1 1829 -> 2656 us at
+// 128 x 1024^2), so the M = 1024 split passes stay.
+#ifndef FDG_QSPLIT_LMAX
+#define FDG_QSPLIT_LMAX 1024
+#endif
+template <int L, bool ROWS>
+struct UseQ {
+  static constexpr bool value = FDG_QSPLIT && (L == 1024 || L == 2048) && L <= FDG_QSPLIT_LMAX && QCfg<L, ROWS>::OK;
+};
+
+template <int L, int MODE>
+cudaError_t run_rowq(cudaStream_t st, const RowArgs& a) {
+  using Cf = QCfg<L, true>;
+  constexpr size_t SM = RowQPlan<L, MODE, true>::SMEM;
+  int cap = 0;
+  cudaError_t e = prep<k_rowq<L, MODE>>(SM, Cf::THREADS, cap);
+  if (e != cudaSuccess) return e;
+  const long F = (long)a.nt * a.n1;
+  return pdl_launch(k_rowq<L, MODE>, clamp_grid(F / (2 * Cf::G), cap), Cf::THREADS, SM, st, a);
+}
+
 template <int L, int MODE>
 cudaError_t run_row(cudaStream_t st, const RowArgs& a) {
+  if constexpr (UseQ<L, true>::value) {
+    if (2 * a.n == L && a.n1 % (2 * QCfg<L, true>::G) == 0 && a.sym_re && a.tw256 && a.twq &&
+        RowQPlan<L, MODE, true>::SMEM <= 227 * 1024)
+      return run_rowq<L, MODE>(st, a);
+  }
   // pipelined full tiles: n == L/2 and tiles of 2G fibres inside one slice
   if constexpr (UseSplit<L>::value) {
     // split passes for full staged tiles; ragged shapes take the direct

@@ -161,6 +161,8 @@ struct RowArgs {
   const double2* twh;    // split passes (fdg_conv.cuh): L/2-point twiddles
   const double2* twist;  // split passes: W_L^j, j < L/2
   const double* sym_re;  // split passes: real symbol (symmetric factor) or null
+  const double2* tw256;  // Q-split passes (fdg_convq.cuh): 256-point plan
+  const double2* twq;    // Q-split passes: W_L^k, k < L
 };
 
 // Early exit of a speculatively enqueued PCG kernel (the host enqueues
@@ -380,6 +382,8 @@ struct ColArgs {
   const double2* twh;    // split passes (fdg_conv.cuh)
   const double2* twist;
   const double* sym_re;
+  const double2* tw256;  // Q-split passes (fdg_convq.cuh)
+  const double2* twq;
 };
 
 template <bool FULL>
