@@ -30,7 +30,7 @@ cudaError_t run_tf(cudaStream_t st, double* data, const PcTables& pt, const int*
 
 // ================================================================ dispatch
 #ifndef FDG_CARVEOUT
-#define FDG_CARVEOUT 1
+#define FDG_CARVEOUT 0
 #endif
 #define FDG_POW2_CASES(X) X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048)
 
@@ -48,8 +48,9 @@ inline cudaError_t prep(size_t smem, int threads, int& grid_cap) {
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (ls.device != dev) {
-    // every pass kernel asks for the max-shared L1 split, so consecutive
-    // kernels of the PCG chain never force an SM reconfiguration drain
+    // FDG_CARVEOUT=1: every pass kernel asks for the max-shared L1 split
+    // (no measurable gain in the C2 chain; costs the L1-resident twiddle
+    // reads of the L = 2048 direct passes, so off by default)
 #if FDG_CARVEOUT
     e = cudaFuncSetAttribute(K, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
