@@ -720,8 +720,9 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
       const double pq = hs[0];
       double rn = std::sqrt(hs[1]);
       if (hs[2] != 0.0) {
-        // iteration it paused the stream: drain the skipped launches
-        ck(cudaStreamSynchronize(st), "drain");
+        // iteration it paused the stream: the speculative launches behind it
+        // exit at their guard; the flag is cleared in stream order after
+        // them (no host drain: the confirmation below queues right behind)
         ck(cudaMemsetAsync(pause, 0, sizeof(int), st), "clear pause");
         if (!std::isfinite(pq) || pq <= 0.0)
           fail(FDG_ENUMERIC, "pcg: operator lost positive definiteness", FDG_NUM_PD_LOSS);
