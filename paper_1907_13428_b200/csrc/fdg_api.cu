@@ -128,6 +128,18 @@ std::vector<double> twiddles(int L) {
 // Per-pass Stockham twiddle table of length N for the device FFT plan
 // (fdg_fft.cuh Stockham: pass with stride Ns > 1 owns (Rp-1)*Ns entries,
 // entry (r-1)*Ns + j = W_N^(j r N/(Ns Rp))).
+// cas(2 pi m / n) = cos + sin, m < n, in long double (dense Hartley path)
+std::vector<double> cas_table(int n) {
+  std::vector<double> c((size_t)n);
+  for (int m = 0; m < n; ++m) {
+    const long double a = 2.0L * kPi * (long double)m / (long double)n;
+    c[m] = (double)(cosl(a) + sinl(a));
+  }
+  return c;
+}
+
+size_t pc_size(int nt, int n1, int n2) { return (size_t)nt * n1 * n2; }
+
 std::vector<double> stockham_twiddles(int N) {
   const std::vector<double> w = twiddles(N);
   std::vector<double> out(2 * (size_t)std::max(N, 1), 0.0);
@@ -425,6 +437,10 @@ struct fdg_pc_s {
   double psi = 1.0, rho = 1.0, delta = 1.0, gamma = 1.0;
   DevBuf lt, l1, l2, twt, tw1, tw2;
   DevBuf work;  // N doubles (standalone solve)
+  // level sizes without a radix plan: dense Hartley axis transforms
+  // (fdg_kernels.cu k_cas_axis), cas tables and an N-double scratch vector
+  bool dense = false;
+  DevBuf cas_t, cas_1, cas_2, dtmp;
   DevBuf pipe;  // nt + 1 counters of the fused axis-pair kernels (null: separate passes)
   PcTables tab;
   // kind 2 (Bluestein passes, fdg_kernels.cu k_bs_*): chirps, real eigenvalues,
@@ -473,6 +489,22 @@ void pc_apply_dev(fdg_pc_s* pc, const double* r, double* z, double* h, const dou
   LaunchCounter* lc = &pc->ctx->lc;
   const int F = pc->nt * pc->n1;
   RedSlot none{};
+  if (pc->dense) {
+    // any level sizes: dense Hartley along x2, x1, t, the 1/(N lambda_S)
+    // scaling, then t, x1, x2 (the last into z; h may alias z)
+    double* tmp = pc->dtmp.d();
+    const int n1 = pc->n1, n2 = pc->n2, nt = pc->nt;
+    const long sl = (long)n1 * n2;
+    ck(fdg::launch_cas_axis(st, lc, r, tmp, (long)nt * n1, n2, 1, pc->cas_2.d()), "pc x2 fwd");
+    ck(fdg::launch_cas_axis(st, lc, tmp, h, nt, n1, n2, pc->cas_1.d()), "pc x1 fwd");
+    ck(fdg::launch_cas_axis(st, lc, h, tmp, 1, nt, sl, pc->cas_t.d()), "pc t fwd");
+    ck(fdg::launch_lams_scale(st, lc, tmp, pc->tab), "pc divide");
+    ck(fdg::launch_cas_axis(st, lc, tmp, h, 1, nt, sl, pc->cas_t.d()), "pc t inv");
+    ck(fdg::launch_cas_axis(st, lc, h, tmp, nt, n1, n2, pc->cas_1.d()), "pc x1 inv");
+    ck(fdg::launch_cas_axis(st, lc, tmp, z, (long)nt * n1, n2, 1, pc->cas_2.d()), "pc x2 inv");
+    if (rdot) ck(fdg::launch_dot(st, lc, rdot, z, pc->N(), red), "pc r.z");
+    return;
+  }
   if (pc->pipe.p) {
     // x2+x1 and x1+x2 pairs fused through L2 (fdg_pcfused.cuh); h != z here
     int* ready = static_cast<int*>(pc->pipe.p);
@@ -1041,10 +1073,11 @@ fdg_pc_s* make_pc(fdg_ctx ctx, int nt, int n1, int n2, const double* lt, const d
                   double psi, double rho, double delta, double gamma) {
   if (!(rho > 0.0) || !(delta > 0.0) || !(gamma > 0.0))
     fail(FDG_EINVAL, "CirculantPreconditioner: scalars must be positive");
-  for (int n : {nt, n1, n2})
-    if (!is_pow2(n) || n > 2048)
-      fail(FDG_EUNSUPPORTED, "fdg: circulant preconditioner needs power-of-two level sizes (got " +
-                                 std::to_string(n) + ")");
+  if (nt < 1 || n1 < 1 || n2 < 1) fail(FDG_EINVAL, "CirculantPreconditioner: level sizes must be positive");
+  // power-of-two levels up to 2048: radix passes; anything else: the dense
+  // Hartley path (same operator)
+  bool dense = false;
+  for (int n : {nt, n1, n2}) dense = dense || !is_pow2(n) || n > 2048;
   // The Hartley formulation needs lambda_S even in every axis: real (hence
   // even) spatial eigenvalues, i.e. symmetric spatial factors.
   for (auto [lam, n] : {std::pair{l1, n1}, std::pair{l2, n2}}) {
@@ -1069,9 +1102,19 @@ fdg_pc_s* make_pc(fdg_ctx ctx, int nt, int n1, int n2, const double* lt, const d
   upload(pc->lt, std::vector<double>(lt, lt + 2 * (size_t)nt), st);
   upload(pc->l1, std::vector<double>(l1, l1 + 2 * (size_t)n1), st);
   upload(pc->l2, std::vector<double>(l2, l2 + 2 * (size_t)n2), st);
-  upload(pc->twt, stockham_twiddles(nt), st);
-  upload(pc->tw1, stockham_twiddles(n1), st);
-  upload(pc->tw2, stockham_twiddles(n2), st);
+  pc->dense = dense;
+  if (dense) {
+    if (std::max(nt, std::max(n1, n2)) > 12288)
+      fail(FDG_EUNSUPPORTED, "fdg: circulant preconditioner level size above 12288");
+    upload(pc->cas_t, cas_table(nt), st);
+    upload(pc->cas_1, cas_table(n1), st);
+    upload(pc->cas_2, cas_table(n2), st);
+    pc->dtmp.alloc(sizeof(double) * pc_size(nt, n1, n2));
+  } else {
+    upload(pc->twt, stockham_twiddles(nt), st);
+    upload(pc->tw1, stockham_twiddles(n1), st);
+    upload(pc->tw2, stockham_twiddles(n2), st);
+  }
   // circulant.cpp:37-40
   const double m2 = 1.0 / (rho * (gamma / (psi * psi) + 1.0 / delta)) + delta / rho;
   PcTables& t = pc->tab;
@@ -1088,7 +1131,7 @@ fdg_pc_s* make_pc(fdg_ctx ctx, int nt, int n1, int n2, const double* lt, const d
   t.base = rho * (1.0 + 1.0 / delta);
   t.inv_m2 = 1.0 / m2;
   t.inv_total = 1.0 / (double)pc->N();
-  if (fdg::pc_pipe_supported(n1, n2)) {
+  if (!dense && fdg::pc_pipe_supported(n1, n2)) {
     pc->pipe.alloc(sizeof(int) * ((size_t)nt + 1));
     ck(cudaMemsetAsync(pc->pipe.p, 0, sizeof(int) * ((size_t)nt + 1), st), "memset");
     ck(cudaStreamSynchronize(st), "sync");

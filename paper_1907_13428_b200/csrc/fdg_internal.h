@@ -120,6 +120,12 @@ cudaError_t launch_pcg_control(cudaStream_t st, LaunchCounter* lc, const double*
 // ------------------------------------------------------------- elementwise
 cudaError_t launch_copy(cudaStream_t st, LaunchCounter* lc, double* dst, const double* src, size_t N);
 cudaError_t launch_fill(cudaStream_t st, LaunchCounter* lc, double* dst, double v, size_t N);
+// Dense Hartley transform along one axis of length n (stride C, O outer
+// blocks) with the cas table cas[m] = cos(2 pi m/n) + sin(2 pi m/n); and the
+// 1/(N lambda_S) scaling of the 3-level preconditioner (any level sizes).
+cudaError_t launch_cas_axis(cudaStream_t st, LaunchCounter* lc, const double* in, double* out, long O, int n,
+                            long C, const double* cas);
+cudaError_t launch_lams_scale(cudaStream_t st, LaunchCounter* lc, double* h, const PcTables& pt);
 // *flag = 1 when some element of x is not zero (flag is not cleared)
 cudaError_t launch_any_nonzero(cudaStream_t st, LaunchCounter* lc, const double* x, size_t N, int* flag);
 // sum of squares (or dot when b != null) -> red.result[0]

@@ -42,6 +42,66 @@ __global__ void k_copy(double* dst, const double* src, size_t N) {
 __global__ void k_fill(double* dst, double v, size_t N) {
   GRID_STRIDE(i, N) dst[i] = v;
 }
+// 3-level preconditioner for level sizes without a radix plan (any n; the
+// reference's Fft3D takes any n, circulant.cpp:49-67): the same operator
+// H^-1 diag(1 / (N lambda_S)) H axis by axis with dense real Hartley
+// transforms, out[o][k][c] = sum_j cas(2 pi j k / n) in[o][j][c] (cas table
+// in shared memory, O(n) per element): the correctness path for small or
+// irregular grids, not a bandwidth path.
+__global__ void k_cas_axis(const double* in, double* out, long O, int n, long C, const double* cas) {
+  extern __shared__ double tab[];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) tab[i] = cas[i];
+  __syncthreads();
+  GRID_STRIDE(e, (size_t)O * n * C) {
+    const size_t r = e / (size_t)C;
+    const long c = (long)(e - r * (size_t)C);
+    const int k = (int)(r % (size_t)n);
+    const size_t o = r / (size_t)n;
+    const double* src = in + o * (size_t)n * C + c;
+    double acc = 0.0;
+    int m = 0;
+    for (int j = 0; j < n; ++j) {
+      acc = fma(tab[m], src[(size_t)j * C], acc);
+      m += k;
+      if (m >= n) m -= n;
+    }
+    out[e] = acc;
+  }
+}
+
+// h *= 1 / (N lambda_S[k, i, j]) with lambda_S from the three 1-D eigenvalue
+// vectors (circulant.cpp:28-41, 62-64; the formula of k_t_filter).
+__global__ void k_lams_scale(double* h, PcTables pt) {
+  const size_t sl = (size_t)pt.n1 * pt.n2;
+  GRID_STRIDE(e, (size_t)pt.nt * sl) {
+    const int k = (int)(e / sl);
+    const size_t ij = e - (size_t)k * sl;
+    const int i = (int)(ij / pt.n2), j = (int)(ij - (size_t)i * pt.n2);
+    const double2 lt = pt.lam_t[k], l1 = pt.lam_1[i], l2 = pt.lam_2[j];
+    const double bx = pt.psi * (lt.x - (l1.x + l2.x)), by = pt.psi * (lt.y - (l1.y + l2.y));
+    const double ls = pt.base + (bx * bx + by * by) * pt.inv_m2;
+    h[e] *= pt.inv_total / ls;
+  }
+}
+
+cudaError_t launch_cas_axis(cudaStream_t st, LaunchCounter* lc, const double* in, double* out, long O, int n,
+                            long C, const double* cas) {
+  count(lc);
+  const size_t smem = sizeof(double) * (size_t)n;
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(k_cas_axis, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_cas_axis<<<ew_grid((size_t)O * n * C), EW_THREADS, smem, st>>>(in, out, O, n, C, cas);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lams_scale(cudaStream_t st, LaunchCounter* lc, double* h, const PcTables& pt) {
+  count(lc);
+  k_lams_scale<<<ew_grid((size_t)pt.nt * pt.n1 * pt.n2), EW_THREADS, 0, st>>>(h, pt);
+  return cudaGetLastError();
+}
+
 // *flag = 1 if some x[i] is not +-0 (NaN included): norm2(x) != 0 without a
 // reduction (admm.cpp:131), for the host-buffer solve's x0 check.
 __global__ void k_any_nonzero(const double* x, size_t N, int* flag) {

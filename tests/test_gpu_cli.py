@@ -18,7 +18,8 @@ def _rows(path):
         return list(csv.DictReader(fh))
 
 
-@pytest.mark.parametrize("n,extra", [(8, {}), (4, {"ulo": -0.5, "uhi": 0.4, "delta": 0.8}), (16, {})])
+@pytest.mark.parametrize("n,extra", [(8, {}), (4, {"ulo": -0.5, "uhi": 0.4, "delta": 0.8}), (16, {}),
+                                   (6, {"ulo": -0.5, "uhi": 0.4, "delta": 0.8}), (12, {})])
 def test_cli_solve_matches_reference_solve(gpu_ctx, ref, tmp_path, capsys, n, extra):
     from paper_1907_13428_b200 import cli
     from paper_1907_13428_b200 import io as fio

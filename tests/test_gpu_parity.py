@@ -94,7 +94,8 @@ def test_operator_adjoint_identity_large(gpu_ctx):
 
 
 # ------------------------------------------------------ preconditioner
-@pytest.mark.parametrize("n", [1, 2, 4, 8, 16, 32])
+# 3, 5, 6, 12, 17: level sizes without a radix plan take the dense Hartley path
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 8, 12, 16, 17, 32])
 def test_precond_reference_default(gpu_ctx, ref, n):
     from paper_1907_13428_b200 import assemble_precond
     rop = ref.op_spec(0.7, 1.3, 1.3, n)
