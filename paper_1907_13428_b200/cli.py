@@ -2,18 +2,20 @@
 
     python -m paper_1907_13428_b200.cli solve  [--config F] [--n N] [--alpha A] ... [--out DIR] [--dump]
     python -m paper_1907_13428_b200.cli sweep  [same flags; n_sweep / alpha_sweep / delta_sweep lists]
+    python -m paper_1907_13428_b200.cli validate [--cap 4] [--perturb 0] [--seed 1]
     python -m paper_1907_13428_b200.cli bench  [--n 16 32] [--reps 5]
 
-A clone of proj/tools/fdeopt_main.cpp's `solve`, `sweep` and `bench`
-subcommands: the same flags, config-file keys (spec.py), precedence (file,
+A clone of proj/tools/fdeopt_main.cpp's `solve`, `sweep`, `validate` and
+`bench` subcommands: the same flags, config-file keys (spec.py), precedence (file,
 then flags, then $FDEOPT_OUT_DIR for the output directory), stdout summary
 rows, output files (solve_summary.csv, solve_iterations.csv, y.bin / u.bin +
 manifest.txt, sweep_summary.csv; formats in io.py) and exit codes (0 ok,
 1 usage or solver failure, 2 iteration cap).  The solves run the reference's
 own experiment (Caputo time factor, Riesz space factors, its desired state
-and dynamic inner tolerance; spec.solve_spec) on the GPU.  `validate` and
-`diagnose` (dense-oracle suite, symbol / Wiener / clustering diagnostics)
-are outside the hot path and not cloned.
+and dynamic inner tolerance; spec.solve_spec) on the GPU; `validate` runs
+the reference's dense-oracle suite (validation.py) against the B200 path
+(exit 3 on a failed check).  `diagnose` (symbol / Wiener / clustering
+diagnostics) is outside the hot path and not cloned.
 
 sweep: points run one after another on this process's GPU; launched under
 torchrun (one rank per GPU) the points are sharded round-robin over the
@@ -31,7 +33,7 @@ import time
 from . import io as fio
 from .spec import ConfigError, RunConfig, apply_config_entry, parse_bound, parse_config_file, solve_spec
 
-EXIT_OK, EXIT_USAGE, EXIT_ITERCAP = 0, 1, 2  # fdeopt_main.cpp:28-31
+EXIT_OK, EXIT_USAGE, EXIT_ITERCAP, EXIT_VALIDATION = 0, 1, 2, 3  # fdeopt_main.cpp:28-31
 
 
 def _common_flags(p: argparse.ArgumentParser) -> None:
@@ -233,6 +235,15 @@ def cmd_bench(sizes, reps: int) -> int:
     return EXIT_OK
 
 
+def cmd_validate(cap: int, perturb: float, seed: int) -> int:
+    """fdeopt_main.cpp:197-208: the dense-oracle equivalence suite
+    (validation.py) against the B200 path; exit 3 on any failed check."""
+    from .validation import B200Backend, format_report, run_validation
+    results = run_validation(B200Backend(), cap, perturb, seed if seed else 1)
+    print(format_report(results), flush=True)
+    return EXIT_OK if all(r.passed() for r in results) else EXIT_VALIDATION
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="fdeopt-b200", description=(
         "matrix-free ADMM solver for box-constrained optimization governed by a time-dependent 2D "
@@ -242,6 +253,12 @@ def main(argv=None) -> int:
     _common_flags(p_solve)
     p_sweep = sub.add_parser("sweep", help="run a sweep over n/alpha/delta lists")
     _common_flags(p_sweep)
+    p_val = sub.add_parser("validate", help="run the dense-oracle equivalence suite")
+    p_val.add_argument("--cap", type=int, default=4, choices=range(1, 7), metavar="[1-6]",
+                       help="dense size cap (<= 6)")
+    p_val.add_argument("--perturb", type=float, default=0.0,
+                       help="fault-injection hook: perturb a discretization coefficient")
+    p_val.add_argument("--seed", type=int, default=1, help="random seed")
     p_bench = sub.add_parser("bench", help="time apply/precond kernels, report peak RSS")
     p_bench.add_argument("--n", type=int, nargs="+", default=[16, 32])
     p_bench.add_argument("--reps", type=int, default=5)
@@ -261,6 +278,8 @@ def main(argv=None) -> int:
             return cmd_solve(args)
         if args.cmd == "sweep":
             return cmd_sweep(args)
+        if args.cmd == "validate":
+            return cmd_validate(args.cap, args.perturb, args.seed)
         return cmd_bench(args.n, args.reps)
     except (ConfigError, ValueError) as e:
         print(f"error: {e}", file=sys.stderr)

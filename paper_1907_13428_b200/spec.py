@@ -273,7 +273,7 @@ def l2_misfit(y: np.ndarray, n: int) -> float:
     return math.sqrt(float(np.dot(d, d)) * h * h * h)
 
 
-def solve_spec(spec: ProblemSpec, admm: AdmmSettings, ctx=None, callback=None) -> dict:
+def solve_spec(spec: ProblemSpec, admm: AdmmSettings, ctx=None, callback=None, keep_state=False) -> dict:
     """fdeopt::solve(spec, cfg) (admm.cpp:279-324) on the B200 path.  Returns
     the SolveResult fields the front end reports plus y, u and history."""
     import time
@@ -297,4 +297,6 @@ def solve_spec(spec: ProblemSpec, admm: AdmmSettings, ctx=None, callback=None) -
     y = drv.get("y")
     u = drv.get("v") / psi
     res.update(y=y, u=u, misfit=l2_misfit(y, n), wall_seconds=time.perf_counter() - t0)
+    if keep_state:  # the rest of SolveResult's state (admm.hpp:45-53)
+        res.update({k: drv.get(k) for k in ("p", "w_y", "w_v", "z_y", "z_v")})
     return res
