@@ -22,7 +22,7 @@ static cudaError_t run_pipe(cudaStream_t st, const PipeArgs& a) {
   int cap = 0;
   cudaError_t e = prep<k_pc_pipe<N>>(P::SMEM, P::THREADS, cap);
   if (e != cudaSuccess) return e;
-  return pdl_launch(k_pc_pipe<N>, (unsigned)cap, P::THREADS, P::SMEM, st, a);
+  return pdl_launch(PDL_MISC, k_pc_pipe<N>, (unsigned)cap, P::THREADS, P::SMEM, st, a);
 }
 
 cudaError_t launch_pc_pipe(cudaStream_t st, LaunchCounter* lc, const double* in, double* mid, double* out,

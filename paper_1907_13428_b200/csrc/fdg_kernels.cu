@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "fdg_fft.cuh"
 #include "fdg_internal.h"
@@ -488,7 +489,22 @@ cudaError_t launch_pcg_control(cudaStream_t st, LaunchCounter* lc, const double*
     dev_set = dev;
   }
 #endif
-  return pdl_launch(k_pcg_control, 1, 1, 0, st, pq, rr, tol_nb2, out, pause, guard, seq);
+  return pdl_launch(PDL_MISC, k_pcg_control, 1, 1, 0, st, pq, rr, tol_nb2, out, pause, guard, seq);
+}
+
+bool pdl_after(bool l1) {
+  thread_local bool last_l1 = false;
+  const bool ok = !l1 || last_l1;
+  last_l1 = l1;
+  return ok;
+}
+
+int pdl_mask() {
+  static const int m = [] {
+    const char* e = std::getenv("FDG_PDL_MASK");
+    return e ? std::atoi(e) : -1;
+  }();
+  return m;
 }
 
 cudaError_t launch_copy(cudaStream_t st, LaunchCounter* lc, double* dst, const double* src, size_t N) {
@@ -522,7 +538,7 @@ cudaError_t launch_cg_update(cudaStream_t st, LaunchCounter* lc, double* x, doub
 cudaError_t launch_axpy_dev(cudaStream_t st, LaunchCounter* lc, double* x, const double* p, size_t N,
                             const double* a_num, const double* a_den, const int* guard) {
   count(lc);
-  return pdl_launch(k_axpy_dev, ew_grid(N), EW_THREADS, 0, st, x, p, N, a_num, a_den, guard);
+  return pdl_launch(PDL_MISC, k_axpy_dev, ew_grid(N), EW_THREADS, 0, st, x, p, N, a_num, a_den, guard);
 }
 cudaError_t launch_residual(cudaStream_t st, LaunchCounter* lc, double* r, const double* b, const double* q,
                             size_t N, RedSlot red) {

@@ -29,6 +29,9 @@ template <int N>
 cudaError_t run_tf(cudaStream_t st, double* data, const PcTables& pt, const int* guard);
 
 // ================================================================ dispatch
+#ifndef FDG_PDL
+#define FDG_PDL 1
+#endif
 #ifndef FDG_CARVEOUT
 #define FDG_CARVEOUT 0
 #endif
@@ -78,8 +81,21 @@ inline void count(LaunchCounter* lc, unsigned long long k = 1) {
 // Launch with programmatic stream serialization (PDL): the kernel may begin
 // while its predecessor drains; it synchronizes with griddepcontrol.wait
 // (fdg_passes.cuh pdl_wait) before touching the predecessor's outputs.
+// Launch classes for the programmatic-dependent-launch policy (pdl_mask):
+// 1 K row passes, 2 K column passes, 4 P row passes, 8 P column passes,
+// 16 t filter, 32 control / axpy / pipe.
+// PDL_L1 marks unstaged variants, whose loads and twiddles go through L1:
+// launched programmatically right behind a kernel with a large shared-memory
+// footprint they inherit that SM configuration (a small L1) instead of the
+// L1-heavy one the driver picks for an idle SM (measured at 128 x 1024^2:
+// the unstaged x1 pass K2 behind K1 loses 1.4 ms per iteration), so they use
+// PDL only right behind another unstaged kernel.
+enum PdlClass { PDL_KROW = 1, PDL_KCOL = 2, PDL_PROW = 4, PDL_PCOL = 8, PDL_TF = 16, PDL_MISC = 32, PDL_L1 = 64 };
+int pdl_mask();             // fdg_kernels.cu: FDG_PDL_MASK (env) or the default
+bool pdl_after(bool l1);    // fdg_kernels.cu: whether PDL may be used, records this launch
+
 template <typename... KArgs, typename... Args>
-inline cudaError_t pdl_launch(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem,
+inline cudaError_t pdl_launch(int cls, void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem,
                               cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -90,7 +106,8 @@ inline cudaError_t pdl_launch(void (*kernel)(KArgs...), unsigned grid, unsigned 
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  const bool after = pdl_after((cls & PDL_L1) != 0);
+  cfg.numAttrs = (FDG_PDL && (pdl_mask() & cls & 63) && after) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
@@ -119,7 +136,7 @@ cudaError_t run_rowc_s(cudaStream_t st, const RowArgs& a) {
   cudaError_t e = prep<k_rowc<L, MODE, PF, SR>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
   const long F = (long)a.nt * a.n1;
-  return pdl_launch(k_rowc<L, MODE, PF, SR>, clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st,
+  return pdl_launch(PDL_KROW, k_rowc<L, MODE, PF, SR>, clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st,
                     a);
 }
 
@@ -131,7 +148,7 @@ cudaError_t run_colc_s(cudaStream_t st, const ColArgs& a) {
   cudaError_t e = prep<k_colc<L, MODE, PF, SR>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
   const long tiles = (long)a.O * ((a.C + 2 * Cf::G - 1) / (2 * Cf::G));
-  return pdl_launch(k_colc<L, MODE, PF, SR>, clamp_grid(tiles, cap), Cf::THREADS, SM, st, a);
+  return pdl_launch(PDL_KCOL, k_colc<L, MODE, PF, SR>, clamp_grid(tiles, cap), Cf::THREADS, SM, st, a);
 }
 
 constexpr size_t kMaxSmem = 227 * 1024;
@@ -145,7 +162,7 @@ cudaError_t run_row_direct(cudaStream_t st, const RowArgs& a) {
   cudaError_t e = prep<k_row<L, MODE, PF>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
   const long F = (long)a.nt * a.n1;
-  return pdl_launch(k_row<L, MODE, PF>, clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st, a);
+  return pdl_launch(PDL_KROW | (PF ? 0 : PDL_L1), k_row<L, MODE, PF>, clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st, a);
 }
 template <int L, int MODE, bool PF>
 cudaError_t run_row_v(cudaStream_t st, const RowArgs& a) {
@@ -176,7 +193,7 @@ cudaError_t run_rowq(cudaStream_t st, const RowArgs& a) {
   cudaError_t e = prep<k_rowq<L, MODE>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
   const long F = (long)a.nt * a.n1;
-  return pdl_launch(k_rowq<L, MODE>, clamp_grid(F / (2 * Cf::G), cap), Cf::THREADS, SM, st, a);
+  return pdl_launch(PDL_KROW, k_rowq<L, MODE>, clamp_grid(F / (2 * Cf::G), cap), Cf::THREADS, SM, st, a);
 }
 
 template <int L, int MODE>
@@ -214,7 +231,7 @@ cudaError_t run_col_direct(cudaStream_t st, const ColArgs& a) {
   cudaError_t e = prep<k_col<L, MODE, PF>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
   const long tiles = (long)a.O * ((a.C + 2 * Cf::G - 1) / (2 * Cf::G));
-  return pdl_launch(k_col<L, MODE, PF>, clamp_grid(tiles, cap), Cf::THREADS, SM, st, a);
+  return pdl_launch(PDL_KCOL | (PF ? 0 : PDL_L1), k_col<L, MODE, PF>, clamp_grid(tiles, cap), Cf::THREADS, SM, st, a);
 }
 template <int L, int MODE, bool PF>
 cudaError_t run_col_v(cudaStream_t st, const ColArgs& a) {
@@ -256,7 +273,7 @@ cudaError_t run_hrow_v(cudaStream_t st, const double* in, double* out, int F, co
   int cap = 0;
   cudaError_t e = prep<k_hartley_row<N, PF>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
-  return pdl_launch(k_hartley_row<N, PF>, clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st,
+  return pdl_launch(PDL_PROW | (PF ? 0 : PDL_L1), k_hartley_row<N, PF>, clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st,
                     in, out, F, tw, rdot, red, guard);
 }
 
@@ -280,7 +297,7 @@ cudaError_t run_hcol_v(cudaStream_t st, double* data, int O, int C, const double
   cudaError_t e = prep<k_hartley_col<N, PF>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
   const long tiles = (long)O * ((C + 2 * Cf::G - 1) / (2 * Cf::G));
-  return pdl_launch(k_hartley_col<N, PF>, clamp_grid(tiles, cap), Cf::THREADS, SM, st, data, O, C, tw, guard);
+  return pdl_launch(PDL_PCOL | (PF ? 0 : PDL_L1), k_hartley_col<N, PF>, clamp_grid(tiles, cap), Cf::THREADS, SM, st, data, O, C, tw, guard);
 }
 
 template <int N>
@@ -299,7 +316,7 @@ cudaError_t run_tf_v(cudaStream_t st, double* data, const PcTables& pt, const in
   cudaError_t e = prep<k_t_filter<N, PF>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
   const long C = (long)pt.n1 * pt.n2;
-  return pdl_launch(k_t_filter<N, PF>, clamp_grid((C + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st, data,
+  return pdl_launch(PDL_TF | (PF ? 0 : PDL_L1), k_t_filter<N, PF>, clamp_grid((C + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st, data,
                     pt, guard);
 }
 
