@@ -242,7 +242,7 @@ cudaError_t run_col_v(cudaStream_t st, const ColArgs& a) {
 #define FDG_PF_COL2048 0  // 1: spills at 128 registers (measured 4.1 vs 3.2 ms at C4)
 #endif
 #ifndef FDG_SPLIT_COL_LMAX
-#define FDG_SPLIT_COL_LMAX 1024  // L = 2048 column tiles (W = 4) lose to the direct kernel
+#define FDG_SPLIT_COL_LMAX 2048  // L = 2048 split column tiles (W = 4): K2 3195 -> 3169 us at C4 in the chain
 #endif
 template <int L, int MODE>
 cudaError_t run_col(cudaStream_t st, const ColArgs& a) {
