@@ -30,6 +30,12 @@ namespace fdg {
 // Tile configuration for transform length L.
 //   R: complex values per thread, T = L/R threads per lane, G lanes per CTA
 //   (256 threads), DB: double-buffered exchanges, TS: twiddles in smem.
+#ifndef FDG_T128_THREADS
+#define FDG_T128_THREADS 128
+#endif
+#ifndef FDG_T128_MINB
+#define FDG_T128_MINB 3
+#endif
 #ifndef FDG_T256_THREADS
 #define FDG_T256_THREADS 128
 #endif
@@ -55,10 +61,10 @@ template <int L>
 struct Cfg {
   static constexpr int R = fft_radix(L);
   static constexpr int T = L / R;
-  static constexpr int G_ = (L == 256 ? FDG_T256_THREADS : (L == 512 ? FDG_T512_THREADS : 256)) / T;
+  static constexpr int G_ = (L == 128 ? FDG_T128_THREADS : (L == 256 ? FDG_T256_THREADS : (L == 512 ? FDG_T512_THREADS : 256))) / T;
   static constexpr int G = G_ > 32 ? 32 : (G_ < 2 ? 2 : G_);
   static constexpr int THREADS = G * T;
-  static constexpr int MINB = L == 256 ? FDG_T256_MINB : (L == 512 ? FDG_T512_MINB : 2);
+  static constexpr int MINB = L == 128 ? FDG_T128_MINB : (L == 256 ? FDG_T256_MINB : (L == 512 ? FDG_T512_MINB : 2));
   static constexpr bool DB = L == 256 ? (FDG_T256_DB != 0) : (L == 512 ? (FDG_T512_DB != 0) : L <= 512);
   static constexpr bool TS = L <= 1024;
   static constexpr size_t EXB = (size_t)L * G;  // double2 per exchange buffer
