@@ -53,6 +53,12 @@ namespace fdg {
 #ifndef FDG_C512_MINB_COL
 #define FDG_C512_MINB_COL 2
 #endif
+#ifndef FDG_C1024_THREADS
+#define FDG_C1024_THREADS 256
+#endif
+#ifndef FDG_C1024_MINB_COL
+#define FDG_C1024_MINB_COL 1
+#endif
 #ifndef FDG_C_HOMO
 #define FDG_C_HOMO 1
 #endif
@@ -72,12 +78,12 @@ struct CCfg {
   static constexpr int R = fft_radix(M);
   static constexpr int T = M / R;   // threads per sub-lane
   static constexpr int LT = 2 * T;  // threads per lane
-  static constexpr int THREADS_ = L == 512 ? FDG_C512_THREADS : 256;
+  static constexpr int THREADS_ = L == 512 ? FDG_C512_THREADS : (L == 1024 ? FDG_C1024_THREADS : 256);
   static constexpr int G = THREADS_ / LT < 1 ? 1 : THREADS_ / LT;  // lanes per CTA
   static constexpr int G2 = 2 * G;                                 // sub-lanes per CTA
   static constexpr int THREADS = G * LT;
   static constexpr int MINB_ROW = L == 512 ? FDG_C512_MINB_ROW : 1;
-  static constexpr int MINB_COL = L == 512 ? FDG_C512_MINB_COL : 1;
+  static constexpr int MINB_COL = L == 512 ? FDG_C512_MINB_COL : (L == 1024 ? FDG_C1024_MINB_COL : 1);
   static constexpr int HR = R / 2;               // output positions per thread
   static constexpr size_t EXB = (size_t)M * G2;  // double2, one exchange buffer
   static constexpr bool HOMO = FDG_C_HOMO != 0;          // rows
