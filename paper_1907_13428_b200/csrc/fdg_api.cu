@@ -664,10 +664,22 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
   Scalars& sc = a->sc;
   fdg_pcg_result res{0, 0, 0.0, 0.0};
   ck(cudaEventRecord(a->e0, st), "event");
+  // |rhs|^2 and |x|^2 in one pass (admm.cpp:124, 131); the host reads them
+  // through an event while the GPU already runs the preconditioner on b,
+  // i.e. speculatively on the x = 0 branch r = b (admm.cpp:131-132) of the
+  // fused schedule; any other branch discards that work below.
+  const bool fused = a->op->tf.kind != 2;
+  ck(fdg::launch_norms2(st, lc, rhs, x, N, sc.slot(S_NB)), "nb xx");
+  ck(cudaMemcpyAsync(ctx->pinned, sc.at(S_NB), 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "norms D2H");
+  ck(cudaEventRecord(a->e2, st), "event");
+  int* pause = static_cast<int*>(a->ctl.p);
+  if (fused) {
+    ck(cudaMemsetAsync(pause, 0, sizeof(int), st), "clear pause");
+    pc_apply_dev(a->pc, rhs, a->z.d(), a->u.d(), rhs, sc.slot(S_RZ0));  // r.z of iteration 1 (odd: S_RZ0)
+  }
+  ck(cudaEventSynchronize(a->e2), "norms");
   double h[2];
-  ck(fdg::launch_dot(st, lc, rhs, nullptr, N, sc.slot(S_NB)), "nb");
-  ck(fdg::launch_dot(st, lc, x, nullptr, N, sc.slot(S_XX)), "xx");
-  sc.read(S_NB, 2, h);
+  std::memcpy(h, ctx->pinned, sizeof(h));
   const double nb = std::sqrt(h[0]);
   auto finish = [&]() {
     ck(cudaEventRecord(a->e1, st), "event");
@@ -684,7 +696,6 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
   }
   // x = 0: r = b; the fused schedule reads b in place of r until the first
   // residual update (no copy)
-  const bool fused = a->op->tf.kind != 2;
   const bool r_is_b = std::sqrt(h[1]) == 0.0 && fused;
   if (std::sqrt(h[1]) == 0.0) {
     if (!fused) ck(fdg::launch_copy(st, lc, a->r.d(), rhs, N), "r = b");
@@ -706,8 +717,6 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
     // re-enqueues.  Iteration parity fixes the ping-pong buffers and slots.
     fdg_op_s* op = a->op;
     const TimeFactor& tf = op->tf;
-    int* pause = static_cast<int*>(a->ctl.p);
-    ck(cudaMemsetAsync(pause, 0, sizeof(int), st), "clear pause");
     auto slot_cur = [](int it) { return (it & 1) ? S_RZ0 : S_RZ1; };  // r.z used by iteration it
     auto slot_prv = [](int it) { return (it & 1) ? S_RZ1 : S_RZ0; };
     auto dir_cur = [&](int it) { return (it & 1) ? a->d.d() : a->d2.d(); };
@@ -742,8 +751,7 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
          "control");
       pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(prv), pause);  // r.z' -> prv slot
     };
-    const double* r0 = r_is_b ? rhs : a->r.d();
-    pc_apply_dev(a->pc, r0, a->z.d(), a->u.d(), r0, sc.slot(slot_cur(1)));
+    if (!r_is_b) pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(slot_cur(1)));
     if (max_inner >= 1) enqueue(1, true);
     for (int it = 1; it <= max_inner; ++it) {
       if (it < max_inner) enqueue(it + 1, true);  // speculative

@@ -129,6 +129,9 @@ cudaError_t launch_lams_scale(cudaStream_t st, LaunchCounter* lc, double* h, con
 // *flag = 1 when some element of x is not zero (flag is not cleared)
 cudaError_t launch_any_nonzero(cudaStream_t st, LaunchCounter* lc, const double* x, size_t N, int* flag);
 // sum of squares (or dot when b != null) -> red.result[0]
+// |a|^2, |b|^2 -> red.result[0..1] (one pass; partials need 2 x grid)
+cudaError_t launch_norms2(cudaStream_t st, LaunchCounter* lc, const double* a, const double* b, size_t N,
+                          RedSlot red);
 cudaError_t launch_dot(cudaStream_t st, LaunchCounter* lc, const double* a, const double* b, size_t N,
                        RedSlot red);
 // x += alpha p (alpha = num/den, optional), p = z + beta p (beta = bnum/bden)

@@ -525,6 +525,25 @@ cudaError_t launch_any_nonzero(cudaStream_t st, LaunchCounter* lc, const double*
   k_any_nonzero<<<ew_grid(N), EW_THREADS, 0, st>>>(x, N, flag);
   return cudaGetLastError();
 }
+// |a|^2 and |b|^2 in one pass, into red.result[0], red.result[1]
+__global__ void k_norms2(const double* a, const double* b, size_t N, RedSlot red) {
+  __shared__ double scratch[64];
+  double sa = 0.0, sb = 0.0;
+  GRID_STRIDE(i, N) {
+    const double u = a[i], v = b[i];
+    sa += u * u;
+    sb += v * v;
+  }
+  double vv[2] = {sa, sb};
+  block_reduce<RED_SUM, 2>(vv, scratch);
+  grid_finalize<RED_SUM, 2>(vv, red, scratch);
+}
+cudaError_t launch_norms2(cudaStream_t st, LaunchCounter* lc, const double* a, const double* b, size_t N,
+                          RedSlot red) {
+  count(lc);
+  k_norms2<<<ew_grid(N), EW_THREADS, 0, st>>>(a, b, N, red);
+  return cudaGetLastError();
+}
 cudaError_t launch_dot(cudaStream_t st, LaunchCounter* lc, const double* a, const double* b, size_t N,
                        RedSlot red) {
   count(lc);
