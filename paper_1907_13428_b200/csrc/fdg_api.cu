@@ -651,6 +651,10 @@ void wait_status(cudaStream_t st, const volatile double* hs, double seq) {
   std::atomic_thread_fence(std::memory_order_acquire);
 }
 
+#ifndef FDG_PCG_SPECULATE
+#define FDG_PCG_SPECULATE 0
+#endif
+
 // pcg (admm.cpp:121-169) with apply = apply_S, precond = pc.solve.
 // on_final_x (optional): called right after the x update that precedes a
 // true-residual confirmation is enqueued (x then holds the candidate result;
@@ -754,7 +758,12 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
     if (!r_is_b) pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(slot_cur(1)));
     if (max_inner >= 1) enqueue(1, true);
     for (int it = 1; it <= max_inner; ++it) {
-      if (it < max_inner) enqueue(it + 1, true);  // speculative
+      // FDG_PCG_SPECULATE: enqueue iteration it+1 before reading iteration
+      // it's status.  Off by default: the host reads the status right after
+      // the control step and enqueues it+1 while the GPU still runs the ~0.3
+      // ms preconditioner of it, so nothing is lost, and at convergence no
+      // speculative iteration has to drain through its guards.
+      if (FDG_PCG_SPECULATE && it < max_inner) enqueue(it + 1, true);
       const volatile double* hs = a->hstat + 4 * (it & 1);
       wait_status(st, hs, a->hseq[it & 1]);
       const double pq = hs[0];
@@ -785,6 +794,8 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
         // continue (from the replaced residual): the skipped tail of it, then it+1
         pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(slot_prv(it)));
         if (it < max_inner) enqueue(it + 1, true);
+      } else if (!FDG_PCG_SPECULATE && it < max_inner) {
+        enqueue(it + 1, true);
       }
     }
     if (max_inner >= 1 && x_host != max_inner) x_update(max_inner);  // no K1F carries the last update
