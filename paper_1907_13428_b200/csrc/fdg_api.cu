@@ -557,6 +557,7 @@ struct fdg_admm_s {
   // its nonzero flag (allocated on first use)
   cudaStream_t cstream = nullptr;
   cudaEvent_t ev_x0 = nullptr;
+  cudaEvent_t ev_norms = nullptr;  // pcg_dev: |rhs|^2, |x|^2 landed on the host
   DevBuf x0buf, x0flag;
   int* x0flag_host = nullptr;  // pinned
   double seq = 0.0;
@@ -675,13 +676,13 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
   const bool fused = a->op->tf.kind != 2;
   ck(fdg::launch_norms2(st, lc, rhs, x, N, sc.slot(S_NB)), "nb xx");
   ck(cudaMemcpyAsync(ctx->pinned, sc.at(S_NB), 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "norms D2H");
-  ck(cudaEventRecord(a->e2, st), "event");
+  ck(cudaEventRecord(a->ev_norms, st), "event");
   int* pause = static_cast<int*>(a->ctl.p);
   if (fused) {
     ck(cudaMemsetAsync(pause, 0, sizeof(int), st), "clear pause");
     pc_apply_dev(a->pc, rhs, a->z.d(), a->u.d(), rhs, sc.slot(S_RZ0));  // r.z of iteration 1 (odd: S_RZ0)
   }
-  ck(cudaEventSynchronize(a->e2), "norms");
+  ck(cudaEventSynchronize(a->ev_norms), "norms");
   double h[2];
   std::memcpy(h, ctx->pinned, sizeof(h));
   const double nb = std::sqrt(h[0]);
@@ -1379,6 +1380,7 @@ fdg_status fdg_admm_create(fdg_op op, fdg_pc pc, const fdg_admm_desc* desc, cons
     a->sc.init(ctx);
     a->inner_tol = d.inner_tol_factor * d.inner_tol_floor;  // admm.cpp:245
     for (cudaEvent_t* e : {&a->e0, &a->e1, &a->e2, &a->e3}) ck(cudaEventCreate(e), "event");
+    ck(cudaEventCreateWithFlags(&a->ev_norms, cudaEventDisableTiming), "event");
     a->ctl.alloc(sizeof(int) * 4);
     ck(cudaMemsetAsync(a->ctl.p, 0, sizeof(int) * 4, st), "memset");
     ck(cudaHostAlloc(&a->hstat, sizeof(double) * 8, cudaHostAllocMapped), "pinned status");
@@ -1394,7 +1396,7 @@ fdg_status fdg_admm_destroy(fdg_admm a) {
     if (!a) return;
     a->op->ctx->set_device();
     cudaStreamSynchronize(a->op->ctx->stream);
-    for (cudaEvent_t e : {a->e0, a->e1, a->e2, a->e3, a->ev_x0})
+    for (cudaEvent_t e : {a->e0, a->e1, a->e2, a->e3, a->ev_x0, a->ev_norms})
       if (e) cudaEventDestroy(e);
     if (a->cstream) cudaStreamDestroy(a->cstream);
     if (a->x0flag_host) cudaFreeHost(a->x0flag_host);
