@@ -172,6 +172,9 @@ cudaError_t run_row_v(cudaStream_t st, const RowArgs& a) {
 #ifndef FDG_QSPLIT
 #define FDG_QSPLIT 1
 #endif
+#ifndef FDG_SPLIT_RAGGED
+#define FDG_SPLIT_RAGGED 0
+#endif
 // Q-split passes (fdg_convq.cuh) for full tiles with real symbols.  Rows at
 // L = 1024 only: measured at 128 x 512^2 K3 383 -> 369 us, K1 equal; at
 // L = 2048 (Q = 8) the input/output combinations and the scattered twist
@@ -214,6 +217,12 @@ cudaError_t run_row(cudaStream_t st, const RowArgs& a) {
         if constexpr (RowCPlan<L, MODE, true, false>::SMEM <= kMaxSmem) return run_rowc_s<L, MODE, true, false>(st, a);
       }
     }
+#if FDG_SPLIT_RAGGED
+    if (2 * a.n > L / 2 + 1) {  // ragged n (e.g. C1's 1023): unstaged split pass
+      if (a.sym_re) return run_rowc_s<L, MODE, false, true>(st, a);
+      return run_rowc_s<L, MODE, false, false>(st, a);
+    }
+#endif
     return run_row_direct<L, MODE, false>(st, a);
   } else {
     if constexpr (Cfg<L>::PF_OK) {
@@ -254,6 +263,12 @@ cudaError_t run_col(cudaStream_t st, const ColArgs& a) {
         if constexpr (ColCPlan<L, MODE, true, false>::SMEM <= kMaxSmem) return run_colc_s<L, MODE, true, false>(st, a);
       }
     }
+#if FDG_SPLIT_RAGGED
+    if (2 * a.n > L / 2 + 1) {
+      if (a.sym_re) return run_colc_s<L, MODE, false, true>(st, a);
+      return run_colc_s<L, MODE, false, false>(st, a);
+    }
+#endif
     return run_col_direct<L, MODE, false>(st, a);
   } else {
     // staged full tiles for the direct column kernel also at L = 2048 (the
