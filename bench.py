@@ -301,16 +301,22 @@ def run_b200(args):
         p["gbs"] = p["bytes"] / (p["ms"] * 1e-3) / 1e9 if p["ms"] > 0 else None  # 0: fused into a neighbour
     dom_name = max(passes, key=lambda k: passes[k]["ms"])
     dom = passes[dom_name]
-    traffic = None
+    traffic, fp64_pct, issue_pct = None, None, None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(dom_name)
+            nt = json.load(f)
+        traffic = nt.get(dom_name)
+        fp64_pct = nt.get("_fp64_pipe_pct", {}).get(dom_name)
+        issue_pct = nt.get("_issue_active_pct", {}).get(dom_name)
     except Exception:
         pass
     roofline = {"bound": "hbm", "kernel": dom_name, "achieved": dom["gbs"], "peak": peak,
                 "peak_kind": peak_kind, "unit": "GB/s", "frac": dom["gbs"] / peak,
                 "traffic": traffic, "algorithmic_bytes_per_launch": dom["bytes"],
-                "avg_launch_ms": dom["ms"]}
+                "avg_launch_ms": dom["ms"],
+                # from the committed ncu capture: the dominant pass is bound by
+                # FP64 latency and shared-memory phases, not by HBM
+                "ncu_fp64_pipe_pct": fp64_pct, "ncu_issue_active_pct": issue_pct}
     it_ms = t_max / max(1.0, it_sum / world)
     iter_roof = {"model": "27 x 8 x N bytes per Krylov iteration (SURVEY.md 8d)",
                  "bytes": B_IT_VECTORS * 8.0 * N, "ms_per_iteration": it_ms,
