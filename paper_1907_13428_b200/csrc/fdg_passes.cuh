@@ -183,7 +183,14 @@ __device__ __forceinline__ bool paused(const int* guard) {
 // their twiddle tables) while the previous kernel drains its last tiles;
 // griddepcontrol.wait then blocks until the previous grid's memory is
 // visible.  Both are no-ops for a normal launch.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::); }
+#ifndef FDG_EARLY_TRIGGER
+#define FDG_EARLY_TRIGGER 1
+#endif
+__device__ __forceinline__ void pdl_trigger() {
+#if FDG_EARLY_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;\n" ::);
+#endif
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
 template <int L, int MODE, bool PF>
