@@ -31,7 +31,7 @@ import sys
 import time
 
 from . import io as fio
-from .spec import ConfigError, RunConfig, apply_config_entry, parse_bound, parse_config_file, solve_spec
+from .spec import ConfigError, RunConfig, parse_bound, parse_config_file, solve_spec
 
 EXIT_OK, EXIT_USAGE, EXIT_ITERCAP, EXIT_VALIDATION = 0, 1, 2, 3  # fdeopt_main.cpp:28-31
 
@@ -166,7 +166,6 @@ def cmd_sweep(args) -> int:
         return EXIT_USAGE
     pts = sweep_points(cfg)
     rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
-    dist = None
     if world > 1:
         import torch
         import torch.distributed as dist

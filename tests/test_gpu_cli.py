@@ -5,7 +5,6 @@ Riesz 1.3, its desired state, dynamic inner tolerance) end to end, with the
 output files in the reference's formats."""
 import csv
 import math
-import os
 
 import numpy as np
 import pytest
