@@ -470,8 +470,13 @@ void pc2_apply_dev(fdg_pc_s* pc, const double* r, double* z) {
   double* u = pc->bu.d();
   double* v = pc->bv.d();
   TimeFactor none;
-  ck(fdg::launch_bs_pre_rows(st, lc, r, u, F, n2, c2), "pc2 x2 pre");
-  ck(fdg::launch_row_apply(st, lc, u, v, 1, Fp, n2, pc->bs2, 1.0 / pc->bs2.L, none, 1.0, false), "pc2 x2 conv");
+  if (F == Fp) {  // the pre-chirp rides in the convolution's load (k_row<.., CH>)
+    ck(fdg::launch_row_apply(st, lc, r, v, 1, Fp, n2, pc->bs2, 1.0 / pc->bs2.L, none, 1.0, false, c2),
+       "pc2 x2 pre + conv");
+  } else {
+    ck(fdg::launch_bs_pre_rows(st, lc, r, u, F, n2, c2), "pc2 x2 pre");
+    ck(fdg::launch_row_apply(st, lc, u, v, 1, Fp, n2, pc->bs2, 1.0 / pc->bs2.L, none, 1.0, false), "pc2 x2 conv");
+  }
   ck(fdg::launch_bs_rows_to_cols(st, lc, v, u, F, n1, n2, P2, c2, c1), "pc2 x2 post");
   ck(fdg::launch_col_acc(st, lc, u, nullptr, v, pc->nt, n1, P2, pc->bs1, 1.0 / pc->bs1.L, false), "pc2 x1 conv");
   ck(fdg::launch_bs_cols_filter(st, lc, v, u, pc->nt, n1, n2, P2, c1, pc->lam1.d(), pc->lam2.d()), "pc2 divide");

@@ -61,7 +61,8 @@ struct PcTables {
 // is a stencil (kind 1).  adjoint selects the transposed time stencil.
 cudaError_t launch_row_apply(cudaStream_t st, LaunchCounter* lc, const double* x, double* out, int nt,
                              int n1, int n2, const AxisSym& s2, double scale, const TimeFactor& tf,
-                             double psi, bool adjoint);
+                             double psi, bool adjoint,
+                             const double2* chirp_in = nullptr);
 
 // out = acc + scale * T(x) along an axis of length n with inner count C and
 // outer count O (axis x1: O = nt, C = n2; axis t: O = 1, C = n1*n2).

@@ -272,8 +272,9 @@ static cudaError_t dispatch_col(cudaStream_t st, int L, const ColArgs& a) {
 
 cudaError_t launch_row_apply(cudaStream_t st, LaunchCounter* lc, const double* x, double* out, int nt, int n1,
                              int n2, const AxisSym& s2, double scale, const TimeFactor& tf, double psi,
-                             bool adjoint) {
+                             bool adjoint, const double2* chirp_in) {
   RowArgs a{};
+  a.chirp_in = chirp_in;
   a.x = x;
   a.out = out;
   a.nt = nt;

@@ -154,15 +154,16 @@ cudaError_t run_colc_s(cudaStream_t st, const ColArgs& a) {
 constexpr size_t kMaxSmem = 227 * 1024;
 
 // direct 2n-point passes (fdg_passes.cuh)
-template <int L, int MODE, bool PF>
+template <int L, int MODE, bool PF, bool CH = false>
 cudaError_t run_row_direct(cudaStream_t st, const RowArgs& a) {
   using Cf = Cfg<L>;
   constexpr size_t SM = RowPlan<L, MODE, PF>::SMEM;
   int cap = 0;
-  cudaError_t e = prep<k_row<L, MODE, PF>>(SM, Cf::THREADS, cap);
+  cudaError_t e = prep<k_row<L, MODE, PF, CH>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
   const long F = (long)a.nt * a.n1;
-  return pdl_launch(PDL_KROW | (PF ? 0 : PDL_L1), k_row<L, MODE, PF>, clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st, a);
+  return pdl_launch(PDL_KROW | (PF ? 0 : PDL_L1), k_row<L, MODE, PF, CH>,
+                    clamp_grid((F + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st, a);
 }
 template <int L, int MODE, bool PF>
 cudaError_t run_row_v(cudaStream_t st, const RowArgs& a) {
@@ -201,6 +202,10 @@ cudaError_t run_rowq(cudaStream_t st, const RowArgs& a) {
 
 template <int L, int MODE>
 cudaError_t run_row(cudaStream_t st, const RowArgs& a) {
+  if (a.chirp_in) {  // folded pre-chirp: the unstaged direct MODE 0 pass only
+    if constexpr (MODE == 0) return run_row_direct<L, 0, false, true>(st, a);
+    return cudaErrorNotSupported;
+  }
   if constexpr (UseQ<L, true>::value) {
     if (2 * a.n == L && a.n1 % (2 * QCfg<L, true>::G) == 0 && a.sym_re && a.tw256 && a.twq &&
         RowQPlan<L, MODE, true>::SMEM <= 227 * 1024)

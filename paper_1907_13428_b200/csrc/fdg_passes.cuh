@@ -169,6 +169,7 @@ struct RowArgs {
   const double* sym_re;  // split passes: real symbol (symmetric factor) or null
   const double2* tw256;  // Q-split passes (fdg_convq.cuh): 256-point plan
   const double2* twq;    // Q-split passes: W_L^k, k < L
+  const double2* chirp_in;  // k_row<.., CH>: input times conj(chirp[pos])
 };
 
 // Early exit of a speculatively enqueued PCG kernel (the host enqueues
@@ -204,7 +205,10 @@ struct RowPlan {
   static constexpr size_t SMEM = P::BYTES;
 };
 
-template <int L, int MODE, bool PF>
+// CH (MODE 0, unstaged): the 2-level preconditioner's Bluestein pre-chirp
+// z conj(chirp[pos]) folded into the load (fdg_kernels.cu k_bs_pre_rows);
+// a separate instantiation, so the plain passes keep their code.
+template <int L, int MODE, bool PF, bool CH = false>
 __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_row(RowArgs a) {
   using C = Cfg<L>;
   using RP = RowPlan<L, MODE, PF>;
@@ -310,6 +314,7 @@ __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_row(RowArgs a
             if (va) a.dnew[ra + pos] = z.x;
             if (vb) a.dnew[ra + n + pos] = z.y;
           }
+          if constexpr (CH) z = cmulc(z, __ldg(&a.chirp_in[pos]));
         }
         v[m] = z;
       }
