@@ -171,12 +171,16 @@ def cmd_sweep(args) -> int:
         import torch.distributed as dist
         from .replicas import gather_records, shard
         local = int(os.environ.get("LOCAL_RANK", "0"))
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        own_group = not dist.is_initialized()
+        if own_group:
+            dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
         mine = shard(list(enumerate(pts)), rank, world)
         done = [(i, *_run_point(p)) for i, p in mine]
         allrec = gather_records([(i, vars(r), c) for i, r, c in done], dist)
-        dist.destroy_process_group()
+        if own_group:
+            dist.destroy_process_group()
         allrec.sort(key=lambda t: t[0])
         rows = [fio.SummaryRow(**r) for _, r, _ in allrec]
         codes = [c for _, _, c in allrec]

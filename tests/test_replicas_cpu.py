@@ -47,3 +47,43 @@ def test_shard_single_rank_and_errors():
     assert aggregate(5.0, 2) == (5.0, 2.0)
     with pytest.raises(ValueError):
         shard([1], 2, 2)
+
+
+def _sweep_worker(rank, world, port, cfg_path, out):
+    """cli sweep under 2 gloo ranks with the GPU solve replaced by a stub:
+    points are sharded round-robin, rank 0 prints every row in point order."""
+    import contextlib
+    import io as _io
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1907_13428_b200 import cli
+    from paper_1907_13428_b200 import io as fio
+
+    def fake_point(p):
+        res = {"status": "converged" if p.admm.delta < 1.0 else "itercap", "iterations": int(10 * p.admm.delta),
+               "pcg_avg": float(rank), "misfit": 0.5, "dual_inf": 1e-9, "wall_seconds": 0.0}
+        return fio.make_summary_row(p, p.admm.delta, res), (0 if res["status"] == "converged" else 2)
+    cli._run_point = fake_point
+    buf = _io.StringIO()
+    with contextlib.redirect_stdout(buf):
+        rc = cli.main(["sweep", "--config", cfg_path])
+    out[rank] = (rc, buf.getvalue())
+    dist.destroy_process_group()
+
+
+def test_cli_sweep_sharded_gloo(tmp_path):
+    cfg = tmp_path / "s.cfg"
+    cfg.write_text("n = 4\ndelta_sweep = 0.2, 0.4, 0.8, 1.2, 1.5\n")
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_sweep_worker, args=(2, _free_port(), str(cfg), out), nprocs=2, join=True)
+    rc0, txt0 = out[0]
+    rc1, txt1 = out[1]
+    assert rc1 == 0 and txt1 == ""
+    lines = txt0.strip().splitlines()
+    assert rc0 == 2 and lines[0].startswith("n,N,alpha")
+    rows = [ln.split(",") for ln in lines[1:]]
+    assert [r[6] for r in rows] == ["0.2", "0.4", "0.8", "1.2", "1.5"]
+    assert [r[10] for r in rows] == ["0", "1", "0", "1", "0"]  # pcg_avg = the rank that ran the point
+    assert [r[13] for r in rows] == ["converged"] * 3 + ["itercap"] * 2
