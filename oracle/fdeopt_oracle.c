@@ -6,6 +6,7 @@
 #include "fdeopt_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -153,36 +154,79 @@ void or_op_destroy(or_op* op) {
   free(op);
 }
 
+/* Fibre-parallel loops: the fibres / lines of one mode are independent and
+ * each writes its own output elements, so splitting them over threads gives
+ * results bit-identical to the serial loop (the reductions stay serial). */
+static int g_or_threads = 1;
+void or_set_threads(int t) { g_or_threads = t < 1 ? 1 : t; }
+int or_get_threads(void) { return g_or_threads; }
+
+typedef void (*or_range_fn)(void* ctx, size_t lo, size_t hi);
+typedef struct { or_range_fn fn; void* ctx; size_t lo, hi; } or_task;
+static void* or_task_main(void* p) {
+  or_task* t = (or_task*)p;
+  t->fn(t->ctx, t->lo, t->hi);
+  return NULL;
+}
+static void par_for(size_t n, or_range_fn fn, void* ctx) {
+  int nt = g_or_threads;
+  if ((size_t)nt > n) nt = (int)n;
+  if (nt <= 1) { fn(ctx, 0, n); return; }
+  or_task* tasks = (or_task*)malloc(sizeof(or_task) * (size_t)nt);
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nt);
+  for (int i = 0; i < nt; ++i) {
+    tasks[i].fn = fn; tasks[i].ctx = ctx;
+    tasks[i].lo = n * (size_t)i / (size_t)nt; tasks[i].hi = n * (size_t)(i + 1) / (size_t)nt;
+  }
+  for (int i = 1; i < nt; ++i) pthread_create(&th[i], NULL, or_task_main, &tasks[i]);
+  or_task_main(&tasks[0]);
+  for (int i = 1; i < nt; ++i) pthread_join(th[i], NULL);
+  free(tasks); free(th);
+}
+
 /* toeplitz.cpp:124-172 for one mode: fibre f of mode m starts at base(f) with
  * stride; pack into a 2n row, r2c, x symbol, c2r, out += scale/(2n) * row. */
-static void apply_mode(const or_op* op, int mode, const double* x, double* out,
-                       const mf_cpx* sym, double scale) {
-  const size_t n1 = (size_t)op->n1, n2 = (size_t)op->n2, nt = (size_t)op->nt;
+typedef struct {
+  const or_op* op; int mode; const double* x; double* out; const mf_cpx* sym; double scale;
+} mode_ctx;
+
+static void apply_mode_range(void* vctx, size_t f0, size_t f1) {
+  const mode_ctx* c = (const mode_ctx*)vctx;
+  const or_op* op = c->op;
+  const int mode = c->mode;
+  const size_t n1 = (size_t)op->n1, n2 = (size_t)op->n2;
   const int n = mode == 0 ? op->nt : (mode == 1 ? op->n1 : op->n2);
   const int len = 2 * n, sl = n + 1;
-  const size_t nfib = (size_t)nt * n1 * n2 / (size_t)n;
   const size_t stride = mode == 0 ? n1 * n2 : (mode == 1 ? n2 : 1);
   double* row = (double*)malloc(sizeof(double) * (size_t)len);
   mf_cpx* spec = (mf_cpx*)malloc(sizeof(mf_cpx) * (size_t)sl);
-  const double w = scale / len;
-  for (size_t f = 0; f < nfib; ++f) {
+  const double w = c->scale / len;
+  for (size_t f = f0; f < f1; ++f) {
     size_t base;
     if (mode == 0) base = f;                                  /* f = i*n2 + j */
     else if (mode == 1) base = (f / n2) * n1 * n2 + f % n2;   /* f = k*n2 + j */
     else base = f * n2;                                       /* f = k*n1 + i */
     for (int t = 0; t < len; ++t) row[t] = 0.0;
-    for (int t = 0; t < n; ++t) row[t] = x[base + (size_t)t * stride];
+    for (int t = 0; t < n; ++t) row[t] = c->x[base + (size_t)t * stride];
     mf_r2c(op->rp[mode], row, 1, spec, 1);
     for (int b = 0; b < sl; ++b) {
-      const mf_cpx a = spec[b], s = sym[b];
+      const mf_cpx a = spec[b], s = c->sym[b];
       spec[b].re = a.re * s.re - a.im * s.im;
       spec[b].im = a.re * s.im + a.im * s.re;
     }
     mf_c2r(op->rp[mode], spec, 1, row, 1);
-    for (int t = 0; t < n; ++t) out[base + (size_t)t * stride] += w * row[t];
+    for (int t = 0; t < n; ++t) c->out[base + (size_t)t * stride] += w * row[t];
   }
   free(row);
   free(spec);
+}
+
+static void apply_mode(const or_op* op, int mode, const double* x, double* out,
+                       const mf_cpx* sym, double scale) {
+  const int n = mode == 0 ? op->nt : (mode == 1 ? op->n1 : op->n2);
+  const size_t nfib = (size_t)op->nt * op->n1 * op->n2 / (size_t)n;
+  mode_ctx c = {op, mode, x, out, sym, scale};
+  par_for(nfib, apply_mode_range, &c);
 }
 
 /* toeplitz.cpp:174-182 */
@@ -282,28 +326,37 @@ void or_pc_destroy(or_pc* pc) {
   free(pc);
 }
 
-static void fft3(const or_pc* pc, mf_cpx* d, int inverse) {
+typedef struct { const or_pc* pc; mf_cpx* d; int inverse, axis; } fft3_ctx;
+
+static void fft3_range(void* vctx, size_t l0, size_t l1) {
+  const fft3_ctx* c = (const fft3_ctx*)vctx;
+  const or_pc* pc = c->pc;
   const size_t nt = (size_t)pc->nt, n1 = (size_t)pc->n1, n2 = (size_t)pc->n2;
   const size_t dims[3] = {nt, n1, n2};
-  size_t maxn = nt > n1 ? nt : n1;
-  if (n2 > maxn) maxn = n2;
-  mf_cpx* a = (mf_cpx*)malloc(sizeof(mf_cpx) * 2 * maxn);
-  mf_cpx* b = a + maxn;
-  for (int axis = 2; axis >= 0; --axis) {
-    const mf_plan* p = inverse ? pc->b[axis] : pc->f[axis];
-    const size_t len = dims[axis];
-    const size_t lines = nt * n1 * n2 / len;
-    for (size_t line = 0; line < lines; ++line) {
-      size_t base, stride;
-      if (axis == 2) { base = line * n2; stride = 1; }
-      else if (axis == 1) { base = (line / n2) * n1 * n2 + line % n2; stride = n2; }
-      else { base = line; stride = n1 * n2; }
-      for (size_t t = 0; t < len; ++t) a[t] = d[base + t * stride];
-      mf_exec(p, a, 1, b, 1);
-      for (size_t t = 0; t < len; ++t) d[base + t * stride] = b[t];
-    }
+  const int axis = c->axis;
+  const mf_plan* p = c->inverse ? pc->b[axis] : pc->f[axis];
+  const size_t len = dims[axis];
+  mf_cpx* a = (mf_cpx*)malloc(sizeof(mf_cpx) * 2 * len);
+  mf_cpx* b = a + len;
+  for (size_t line = l0; line < l1; ++line) {
+    size_t base, stride;
+    if (axis == 2) { base = line * n2; stride = 1; }
+    else if (axis == 1) { base = (line / n2) * n1 * n2 + line % n2; stride = n2; }
+    else { base = line; stride = n1 * n2; }
+    for (size_t t = 0; t < len; ++t) a[t] = c->d[base + t * stride];
+    mf_exec(p, a, 1, b, 1);
+    for (size_t t = 0; t < len; ++t) c->d[base + t * stride] = b[t];
   }
   free(a);
+}
+
+static void fft3(const or_pc* pc, mf_cpx* d, int inverse) {
+  const size_t dims[3] = {(size_t)pc->nt, (size_t)pc->n1, (size_t)pc->n2};
+  const size_t N = dims[0] * dims[1] * dims[2];
+  for (int axis = 2; axis >= 0; --axis) {
+    fft3_ctx c = {pc, d, inverse, axis};
+    par_for(N / dims[axis], fft3_range, &c);
+  }
 }
 
 /* circulant.cpp:49-67 */

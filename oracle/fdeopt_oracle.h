@@ -17,6 +17,10 @@ extern "C" {
 #endif
 
 const char* or_last_error(void);
+/* worker threads for the fibre / line loops (default 1; results do not
+ * depend on the count: every fibre writes its own elements) */
+void or_set_threads(int t);
+int or_get_threads(void);
 
 /* problem.cpp:35-45 */
 int or_frac_coeffs(double order, int count, double* out);

@@ -412,11 +412,21 @@ class PortLib(_Lib):
         L.or_build_caputo.argtypes = [C.c_double, C.c_int, C.c_double, _dp, _dp]
         L.or_embed_symbol.argtypes = [C.c_int, _dp, _dp, C.c_int, _dp]
         L.or_tchan.argtypes = [C.c_int, _dp, _dp, _dp, _dp]
+        L.or_set_threads.argtypes = [C.c_int]
+        L.or_get_threads.restype = C.c_int
 
     def frac_coeffs(self, order, count):
         out = np.zeros(count)
         self.check(self.lib.or_frac_coeffs(order, count, _ptr(out)))
         return out
+
+    def set_threads(self, t):
+        """Fibre-parallel operator / preconditioner loops (bit-identical for
+        any count; reductions stay serial)."""
+        self.lib.or_set_threads(int(t))
+
+    def get_threads(self):
+        return int(self.lib.or_get_threads())
 
     def build_riesz(self, beta, n, h):
         col = np.zeros(n)

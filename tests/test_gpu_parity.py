@@ -123,7 +123,10 @@ def test_precond_golden(gpu_ctx, golden, n):
                                    # n1 == n2 in {256, 512}: x2/x1 pairs fused through L2, fewer
                                    # and more slabs than the pipeline lag
                                    (1, 256, 256), (4, 256, 256), (32, 256, 256), (2, 512, 512),
-                                   (16, 512, 512)])
+                                   (16, 512, 512),
+                                   # n_t = 128 / 256: the t filters k_t_filter<128|256> of the
+                                   # timed C3/C4 and C2 configs
+                                   (128, 16, 32), (256, 16, 16), (128, 64, 64), (256, 32, 64)])
 def test_precond_noncube_vs_port(gpu_ctx, port, shape):
     from oracle import implicit_euler
     from paper_1907_13428_b200 import assemble_precond
@@ -203,11 +206,17 @@ def test_admm_five_steps_golden(gpu_ctx, ref, golden, n):
     assert abs(drv.objective() - golden[f"ie{n}_after5_obj"][0]) <= 1e-8 * abs(golden[f"ie{n}_after5_obj"][0])
 
 
-@pytest.mark.parametrize("shape", [(4, 16, 256), (4, 8, 512), (2, 16, 64), (2, 4, 1024)])
+@pytest.mark.parametrize("shape", [(4, 16, 256), (4, 8, 512), (2, 16, 64), (2, 4, 1024),
+                                   # n1 = 256 / 512 / 1024: the split S-mid column passes
+                                   # k_colc<512|1024|2048, 2> the bench times (K2) and the
+                                   # staged row passes k_rowc<512> / k_rowq<1024> / k_rowc<2048>
+                                   (2, 256, 256), (2, 512, 64), (2, 1024, 32), (2, 16, 1024),
+                                   (2, 512, 512)])
 def test_pcg_noncube_vs_port(gpu_ctx, port, shape):
     """PCG on the ADMM normal equations for shapes that select the staged
-    row kernels (tiles inside one slice) and the L >= 1024 single-buffer
-    kernels, against the generalized C restatement."""
+    row kernels (tiles inside one slice), the L >= 1024 single-buffer
+    kernels and the split column passes of the timed configs, against the
+    generalized C restatement: S within 1e-11, Krylov count +-1."""
     from oracle import Shape, baseline_problem
     from oracle.pyoracle import PortAdmm
     from paper_1907_13428_b200 import AdmmConfig, AdmmDriver, assemble_precond

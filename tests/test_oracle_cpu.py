@@ -209,3 +209,57 @@ def test_baseline_mapping():
     assert c["psi"] == pytest.approx(33.0 ** -1.5, rel=1e-15)
     yb = synthetic_ybar("sin", Shape(2, 3, 4))
     assert yb.shape == (24,) and np.isfinite(yb).all()
+
+
+def test_port_threads_bit_identical(port):
+    """The fibre-parallel port (used for the full-size C3/C4 parity tests)
+    gives the serial loop's results bit for bit: operator, adjoint,
+    preconditioner and a PCG solve."""
+    from oracle.pyoracle import PortAdmm
+    shape = (6, 20, 24)
+    c = baseline_problem("C3", Shape(*shape))
+    pop = port.op(shape, c["time"], c["r1"], c["r2"], c["psi"])
+    ppc = pop.assemble_precond(1.0, 1.0, c["gamma"])
+    x = np.random.default_rng(3).standard_normal(pop.size)
+    out = {}
+    t0 = port.get_threads()
+    try:
+        for t in (1, 5):
+            port.set_threads(t)
+            adm = PortAdmm(port, pop, ppc, c["gamma"], 1.0, 1.0, y_lo=c["y"][0], y_hi=c["y"][1],
+                           u_lo=c["u"][0], u_hi=c["u"][1], tol_primal=1e-6, max_inner=400,
+                           fixed_tol=1e-8, ybar=x)
+            y, r = adm.pcg(adm.build_rhs()[0])
+            out[t] = (pop.apply(x), pop.apply(x, True), ppc.solve(x), y, r["iterations"])
+    finally:
+        port.set_threads(t0)
+    for a, b in zip(out[1], out[5]):
+        assert np.array_equal(a, b)
+
+
+def test_numpy_restatement_vs_port(port):
+    """oracle/np_fdeopt.py (pocketfft backend, the noise-floor checker) agrees
+    with the C restatement: operators 1e-14, PCG counts and residuals of
+    three ADMM steps."""
+    from oracle.np_fdeopt import NpAdmm, NpOperator, NpPrecond
+    from oracle.pyoracle import PortAdmm
+    shape = (5, 12, 10)
+    c = baseline_problem("C3", Shape(*shape))
+    op = NpOperator(shape, c["time"], c["r1"], c["r2"], c["psi"])
+    pc = NpPrecond(op, 1.0, 1.0, c["gamma"])
+    pop = port.op(shape, c["time"], c["r1"], c["r2"], c["psi"])
+    ppc = pop.assemble_precond(1.0, 1.0, c["gamma"])
+    x = np.random.default_rng(9).standard_normal(op.size)
+    assert rel(op.apply(x), pop.apply(x)) < 1e-14
+    assert rel(op.apply(x, True), pop.apply(x, True)) < 1e-14
+    assert rel(pc.solve(x), ppc.solve(x)) < 1e-14
+    a = NpAdmm(op, pc, c["gamma"], 1.0, 1.0, y_lo=c["y"][0], y_hi=c["y"][1], u_lo=c["u"][0],
+               u_hi=c["u"][1], ybar=x)
+    b = PortAdmm(port, pop, ppc, c["gamma"], 1.0, 1.0, y_lo=c["y"][0], y_hi=c["y"][1],
+                 u_lo=c["u"][0], u_hi=c["u"][1], tol_primal=1e-6, max_inner=400, fixed_tol=1e-8,
+                 ybar=x)
+    for _ in range(3):
+        s1, s2 = a.step(), b.step()
+        assert abs(s1["inner_iters"] - s2["inner_iters"]) <= 1
+        for k in ("r_eq", "r_u", "dual_inf"):
+            assert abs(s1[k] - s2[k]) <= 1e-10 * abs(s2[k])
