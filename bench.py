@@ -5,8 +5,8 @@ ADMM normal equations at BASELINE config C2 (256^2 x 256, fp64).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
 A step = one PCG solve (tol 1e-8, x0 = 0, reference control flow) of the
-ADMM sub-problem S y = rhs taken after one ADMM step from a zero state, with
-every input resident in HBM.  value = Krylov iterations of the K timed steps /
+ADMM sub-problem S y = rhs of the zero ADMM state (rhs = rho J ybar, the same
+system in both arms), with every input resident in HBM.  value = Krylov iterations of the K timed steps /
 their device time (CUDA events on the library stream, barrier + sync on both
 sides, max over ranks).  e2e = the same through the host-buffer C-ABI call
 (fdg_admm_pcg_host: H2D rhs and x0 from pinned memory, D2H of x).
@@ -16,6 +16,13 @@ value sums iterations over ranks and divides by the slowest rank's time.
 --impl reference: the unchanged reference (oracle/_ref: reference sources +
 FFTW3 shim) on the host cores; a step = exactly one iteration of the
 reference pcg loop body on the same C2 system (bounded CPU sample).
+
+After the headline the same JSON line carries (rank 0, N = 1):
+  admm        C2 ADMM outer steps (build_rhs, PCG, B y, updates, dual_inf)
+  admm_solve  C0: the full ADMM solve to convergence next to the reference's
+  configs     C3 / C4 with their real BASELINE parameters (PCG it/s, 27N
+              roofline per solve and steady state, dominant pass), C1's
+              matvec and 2-level preconditioner vs their 5N / 6N models
 """
 from __future__ import annotations
 
@@ -57,15 +64,29 @@ def _host_cores():
         return os.cpu_count() or 1
 
 
-def _config(shape, extra=None):
-    c = {"workload": f"{WORKLOAD} {shape[1]}x{shape[2]} interior x {shape[0]} implicit-Euler steps: "
-                     "PCG solve of the ADMM normal equations (T. Chan circulant precond, tol 1e-8)",
-         "shape_nt_nx1_nx2": list(shape), "alpha_x": 1.5, "alpha_y": 1.5, "beta_reg": 1e-5,
-         "krylov_tol": 1e-8, "penalty_rho": 1.0, "parallelism": "replicas",
-         "l2": "inputs larger than L2 (each N-vector 134 MB > 126 MB)"}
-    if extra:
-        c.update(extra)
-    return c
+def _config(shape):
+    """The workload description, identical in both arms (--impl b200 / reference)."""
+    return {"workload": f"{WORKLOAD} {shape[1]}x{shape[2]} interior x {shape[0]} implicit-Euler steps: "
+                        "PCG solve of the ADMM normal equations (T. Chan circulant precond, tol 1e-8), "
+                        "sub-problem of the zero ADMM state (rhs = rho J ybar)",
+            "shape_nt_nx1_nx2": list(shape), "alpha_x": 1.5, "alpha_y": 1.5, "beta_reg": 1e-5,
+            "krylov_tol": 1e-8, "penalty_rho": 1.0, "parallelism": "replicas",
+            "l2": "inputs larger than L2 (each N-vector 134 MB > 126 MB)"}
+
+
+def _fftw_note():
+    """Whether the host has a CPU FFTW3 (the reference's FFT library)."""
+    try:
+        out = subprocess.run(["ldconfig", "-p"], capture_output=True, text=True, timeout=10).stdout
+    except Exception:  # noqa: BLE001
+        return "unknown (ldconfig failed)"
+    libs = sorted({ln.split()[0] for ln in out.splitlines() if "fftw3" in ln})
+    cpu = [x for x in libs if not x.startswith("libcufftw")]
+    if cpu:
+        return "host has CPU FFTW3 (" + ", ".join(cpu) + "); the baseline still links the builder's shim"
+    seen = ("ldconfig lists only " + ", ".join(libs) + ", cuFFT's FFTW-API wrapper (a GPU library)"
+            if libs else "ldconfig lists no fftw3 library")
+    return f"no CPU FFTW3 on the host ({seen}): the reference runs on the builder's FFTW3-API shim (oracle/shim)"
 
 
 class ClockSampler:
@@ -127,13 +148,14 @@ class ClockSampler:
 # --------------------------------------------------------------------------
 # reference arm / CPU baseline: the unchanged reference on the host cores
 # --------------------------------------------------------------------------
-def reference_sample(iters: int, warmup: int, shape=(256, 256, 256)):
+def reference_sample(iters: int, warmup: int, shape=(256, 256, 256), threads=None):
     """Times `iters` single iterations of the reference pcg loop body (after
-    `warmup` untimed ones) on the C2 normal equations; returns per-iteration
-    seconds.  The oracle package is used here only as the CPU baseline."""
+    `warmup` untimed ones) on the C2 normal equations of the zero ADMM state
+    (the sub-problem the B200 arm solves); returns per-iteration seconds.
+    The oracle package is used here only as the CPU baseline."""
     from oracle import Shape, baseline_problem, ref_lib, synthetic_ybar
     from oracle.pyoracle import RefAdmm
-    cores = _host_cores()
+    cores = threads or _host_cores()
     R = ref_lib()
     R.set_threads(cores)
     s = Shape(*shape)
@@ -158,6 +180,13 @@ def reference_sample(iters: int, warmup: int, shape=(256, 256, 256)):
     return times, cores
 
 
+def _ref_sample_text(n, shape, warmup, cores):
+    return (f"{n} single iterations of the unchanged reference pcg loop body (apply_S + "
+            f"CirculantPreconditioner::solve + vector algebra, admm.cpp:142-163) on the {tuple(shape)} "
+            f"zero-state sub-problem after {warmup} warm-up iterations; FFT batches of the FFTW3-API "
+            f"shim on {cores} thread(s), the reference's own loops serial")
+
+
 def run_reference(args):
     rank, _, world = _env_rank()
     if rank != 0:
@@ -166,18 +195,15 @@ def run_reference(args):
     times, cores = reference_sample(args.steps, args.warmup, shape)
     total = sum(times)
     value = len(times) / total
-    sample = (f"{len(times)} single iterations of the reference pcg loop body (apply_S + "
-              f"CirculantPreconditioner::solve + vector algebra, admm.cpp:142-163) on the "
-              f"{shape} system after {args.warmup} warm-up iterations; FFTW3 shim with "
-              f"{cores} threads for the FFT batches, reference loops serial")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "it/s",
             "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
             "ms_per_step": 1000.0 * total / len(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded std::mt19937_64 target state)",
+            "data": "synthetic (seeded std::mt19937_64 target state, BASELINE C2 formulas)",
             "config": _config(shape),
             "cpu_baseline": {"value": value, "unit": "it/s", "cores": cores, "kind": "reference",
-                             "sample": sample},
+                             "sample": _ref_sample_text(len(times), shape, args.warmup, cores),
+                             "fftw": _fftw_note()},
             "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -187,6 +213,170 @@ def run_reference(args):
 # --------------------------------------------------------------------------
 # the B200 arm
 # --------------------------------------------------------------------------
+def _traffic(shape):
+    """ncu DRAM bytes / pipe figures of the committed capture for this shape, or {}."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get("x".join(str(v) for v in shape), {})
+    except Exception:  # noqa: BLE001
+        return {}
+
+
+def _pass_roofline(drv, shape, reps, peak, peak_kind):
+    """Per-pass burst timing (CUDA events on the library stream) and the
+    dominant pass's roofline: algorithmic bytes per launch / average launch
+    time vs the measured HBM copy peak."""
+    passes = drv.profile_passes(reps)
+    for p in passes.values():
+        p["gbs"] = p["bytes"] / (p["ms"] * 1e-3) / 1e9 if p["ms"] > 0 else None
+    dom_name = max(passes, key=lambda k: passes[k]["ms"])
+    dom = passes[dom_name]
+    cap = _traffic(shape)
+    roof = {"bound": "hbm", "kernel": dom_name, "achieved": dom["gbs"], "peak": peak,
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": dom["gbs"] / peak,
+            "traffic": cap.get("traffic", {}).get(dom_name),
+            "traffic_source": cap.get("source"),
+            "algorithmic_bytes_per_launch": dom["bytes"], "avg_launch_ms": dom["ms"],
+            "ncu_fp64_pipe_pct": cap.get("fp64_pipe_pct", {}).get(dom_name),
+            "ncu_issue_active_pct": cap.get("issue_active_pct", {}).get(dom_name)}
+    return roof, passes
+
+
+def _steady_state(drv, rhs, x, N, peak, k_lo=4, k_hi=12, reps=3):
+    """Marginal device time of one more Krylov iteration inside a solve
+    (solves capped at k_lo / k_hi iterations with an unreachable tolerance;
+    slope of the medians) and its 27N-model bandwidth."""
+    import torch
+    t_cap = {}
+    for _ in range(reps):
+        for k in (k_lo, k_hi):
+            x.zero_()
+            torch.cuda.current_stream().synchronize()
+            t_cap.setdefault(k, []).append(drv.pcg_dev(rhs, x, 1e-300, k).ms)
+    slope_ms = (statistics.median(t_cap[k_hi]) - statistics.median(t_cap[k_lo])) / (k_hi - k_lo)
+    st = {"method": f"slope of PCG solve time between {k_lo} and {k_hi} capped iterations "
+                    f"(median of {reps}, CUDA events on the library stream)",
+          "ms_per_iteration": slope_ms,
+          "achieved_gbs": B_IT_VECTORS * 8.0 * N / (slope_ms * 1e-3) / 1e9,
+          "fixed_ms_per_solve": statistics.median(t_cap[k_lo]) - k_lo * slope_ms}
+    st["frac"] = st["achieved_gbs"] / peak
+    return st
+
+
+def _zero_state_rhs(drv, N):
+    import torch
+    rhs = torch.empty(N, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    drv.build_rhs_dev(rhs)
+    drv.op.ctx.synchronize()
+    return rhs
+
+
+def measure_config(name, ctx, peak, peak_kind, steps=3, reps=5):
+    """A BASELINE full-solve config with its real parameters: PCG solves of
+    the zero-state sub-problem (device time), the per-solve and steady-state
+    27N roofline, the dominant pass; then 3 ADMM steps."""
+    import torch
+    from paper_1907_13428_b200 import make_problem
+    c, op, pc, drv = make_problem(name, ctx=ctx)
+    shape = tuple(c["shape"])
+    N = op.size
+    rhs = _zero_state_rhs(drv, N)
+    x = torch.zeros_like(rhs)
+    tol, max_inner = c["krylov_tol"], c["max_inner"]
+    drv.pcg_dev(rhs, x, tol, max_inner)  # warm
+    its, ms = 0, 0.0
+    for _ in range(steps):
+        x.zero_()
+        torch.cuda.current_stream().synchronize()
+        r = drv.pcg_dev(rhs, x, tol, max_inner)
+        its += r.iterations
+        ms += r.ms
+    it_ms = ms / its
+    out = {"shape_nt_nx1_nx2": list(shape), "params": {k: c[k] for k in ("ax", "ay", "dx", "dy", "gamma")} |
+           {"u_box": list(c["u"]), "y_box": [str(v) for v in c["y"]], "ybar": c["ybar"]},
+           "krylov_iters_per_s": its / (ms / 1e3), "iters_per_solve": its / steps,
+           "solve_ms": ms / steps,
+           "iteration_roofline": {"bytes": B_IT_VECTORS * 8.0 * N, "ms_per_iteration": it_ms,
+                                  "frac": B_IT_VECTORS * 8.0 * N / (it_ms * 1e-3) / 1e9 / peak},
+           "steady_state_iteration": _steady_state(drv, rhs, x, N, peak)}
+    out["roofline"], out["passes"] = _pass_roofline(drv, shape, reps, peak, peak_kind)
+    recs = [drv.step() for _ in range(3)]
+    out["admm_steps"] = {"steps": 3, "step_ms_mean": statistics.mean(r.step_ms for r in recs),
+                         "pcg_ms_mean": statistics.mean(r.pcg_ms for r in recs),
+                         "inner_iters": [r.inner_iters for r in recs]}
+    del drv, pc, op, rhs, x
+    return out
+
+
+def measure_c1(ctx, peak, reps=5):
+    """BASELINE config 1: the 2-level Toeplitz matvec and the 2-level T. Chan
+    solve on 256 slices of 1023^2 (N = 267,911,424), device time per call vs
+    the SURVEY 8d pass models (matvec 5N, solve 6N doubles)."""
+    import torch
+    from paper_1907_13428_b200 import make_c1, randn
+    op, pc = make_c1(ctx=ctx)
+    N = op.size
+    x = torch.from_numpy(randn(1, N)).cuda()
+    y = torch.empty_like(x)
+    st = torch.cuda.ExternalStream(ctx.stream)
+    torch.cuda.synchronize()
+
+    def timed(fn):
+        for _ in range(2):
+            fn()
+        ctx.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            fn()
+        e1.record(st)
+        ctx.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    t_mv = timed(lambda: op.apply_dev(x, y))
+    t_pc = timed(lambda: pc.solve_dev(x, y))
+    res = {"shape_slices_nx1_nx2": [256, 1023, 1023], "N": N, "matvec_ms": t_mv, "precond_ms": t_pc,
+           "matvec_frac": 5 * 8 * N / (t_mv * 1e-3) / 1e9 / peak,
+           "precond_frac": 6 * 8 * N / (t_pc * 1e-3) / 1e9 / peak,
+           "model": "matvec 5N x 8 B, 2-level solve 6N x 8 B (SURVEY 8d)"}
+    del op, pc, x, y
+    return res
+
+
+def measure_c0_solve(ctx):
+    """BASELINE config 0 full ADMM solve to convergence (the metric's 'ADMM
+    solve time'), next to the unchanged reference's committed run of the same
+    inputs (tests/golden/ref_c0_solve.json: 1 host thread)."""
+    import torch
+    from paper_1907_13428_b200 import make_problem, solve
+    t0 = time.perf_counter()
+    c, op, pc, drv = make_problem("C0", ctx=ctx)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    res = solve(drv)
+    hist = res["history"]
+    out = {"status": res["status"], "admm_steps": res["iterations"],
+           "krylov_total": int(sum(h.inner_iters for h in hist)),
+           "solve_seconds": res["wall_seconds"], "setup_seconds": t_setup,
+           "pcg_seconds": sum(h.pcg_ms for h in hist) / 1e3,
+           "krylov_iters_per_s_inside_pcg": sum(h.inner_iters for h in hist) /
+           max(1e-9, sum(h.pcg_ms for h in hist) / 1e3),
+           "objective": res["objective"], "r_u": hist[-1].r_u, "r_eq": hist[-1].r_eq}
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "ref_c0_solve.json")) as f:
+            ref = json.load(f)
+        out["reference"] = {k: ref[k] for k in ("admm_iterations", "total_krylov", "wall_seconds",
+                                                 "pcg_seconds", "threads", "note")}
+        out["same_counts"] = (out["admm_steps"] == ref["admm_iterations"] and
+                              out["krylov_total"] == ref["total_krylov"])
+        out["speedup_vs_reference_wall"] = ref["wall_seconds"] / out["solve_seconds"]
+    except Exception:  # noqa: BLE001
+        pass
+    del drv, pc, op
+    return out
+
+
 def run_b200(args):
     import torch
     rank, local_rank, world = _env_rank()
@@ -203,13 +393,10 @@ def run_b200(args):
     stream = torch.cuda.ExternalStream(ctx.stream)
     c, op, pc, drv = make_problem(WORKLOAD, shape, ctx=ctx, seed=1 + rank)
 
-    # the hot-path input: the ADMM sub-problem after one step from zero
-    drv.step()
-    rhs = torch.empty(N, dtype=torch.float64, device="cuda")
+    # the hot-path input: the ADMM sub-problem of the zero state (the same
+    # system the reference arm iterates on)
+    rhs = _zero_state_rhs(drv, N)
     x = torch.empty_like(rhs)
-    torch.cuda.synchronize()
-    drv.build_rhs_dev(rhs)
-    ctx.synchronize()
     tol, max_inner = c["krylov_tol"], c["max_inner"]
 
     # x is in/out and every step starts from x0 = 0: the timed steps get
@@ -255,6 +442,7 @@ def run_b200(args):
     launches = ctx.launch_count - l0
     clk = clocks.stop()
     elapsed_ms = ev0.elapsed_time(ev1)
+    del x_pre
 
     from paper_1907_13428_b200.replicas import aggregate
     t_max, it_sum = aggregate(elapsed_ms, iters, dist, "cuda")
@@ -283,71 +471,57 @@ def run_b200(args):
     e2e = {"value": e_it / (e_tmax / 1000.0), "unit": "it/s", "h2d_bytes_per_step": 2 * 8 * N,
            "d2h_bytes_per_step": 8 * N, "steps": e_steps,
            "path": "fdg_admm_pcg_host (pinned host rhs/x0 -> device PCG -> host x)"}
+    del xs, rhs_h
 
-    # ADMM step time (full outer iteration: build_rhs, PCG, B y, updates, dual_inf)
-    admm = None
-    if args.admm_steps > 0:
-        recs = [drv.step() for _ in range(args.admm_steps)]
-        admm = {"steps": len(recs), "step_ms_mean": statistics.mean(r.step_ms for r in recs),
-                "pcg_ms_mean": statistics.mean(r.pcg_ms for r in recs),
-                "inner_iters": [r.inner_iters for r in recs],
-                "r_eq_last": recs[-1].r_eq, "r_u_last": recs[-1].r_u}
-
-    # per-kernel roofline (burst: each pass launched back to back)
     peak, peak_kind = _peaks()
-    passes = drv.profile_passes(args.profile_reps)
-    for p in passes.values():
-        p["gbs"] = p["bytes"] / (p["ms"] * 1e-3) / 1e9 if p["ms"] > 0 else None  # 0: fused into a neighbour
-    dom_name = max(passes, key=lambda k: passes[k]["ms"])
-    dom = passes[dom_name]
-    traffic, fp64_pct, issue_pct = None, None, None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            nt = json.load(f)
-        traffic = nt.get(dom_name)
-        fp64_pct = nt.get("_fp64_pipe_pct", {}).get(dom_name)
-        issue_pct = nt.get("_issue_active_pct", {}).get(dom_name)
-    except Exception:
-        pass
-    roofline = {"bound": "hbm", "kernel": dom_name, "achieved": dom["gbs"], "peak": peak,
-                "peak_kind": peak_kind, "unit": "GB/s", "frac": dom["gbs"] / peak,
-                "traffic": traffic, "algorithmic_bytes_per_launch": dom["bytes"],
-                "avg_launch_ms": dom["ms"],
-                # from the committed ncu capture: the dominant pass is bound by
-                # FP64 latency and shared-memory phases, not by HBM
-                "ncu_fp64_pipe_pct": fp64_pct, "ncu_issue_active_pct": issue_pct}
+    roofline, passes = _pass_roofline(drv, shape, args.profile_reps, peak, peak_kind)
     it_ms = t_max / max(1.0, it_sum / world)
     iter_roof = {"model": "27 x 8 x N bytes per Krylov iteration (SURVEY.md 8d)",
                  "bytes": B_IT_VECTORS * 8.0 * N, "ms_per_iteration": it_ms,
                  "achieved_gbs": B_IT_VECTORS * 8.0 * N / (it_ms * 1e-3) / 1e9}
     iter_roof["frac"] = iter_roof["achieved_gbs"] / peak
-    # steady-state Krylov iteration: the marginal device time of one more
-    # iteration inside a solve (solves capped at k_lo and k_hi iterations with
-    # an unreachable tolerance; slope of the medians), i.e. the iteration's
-    # cost without the per-solve preconditioner start / true-residual check
-    k_lo, k_hi = 4, 12
-    t_cap = {}
-    for _ in range(3):
-        for k in (k_lo, k_hi):
-            x.zero_()
-            torch.cuda.current_stream().synchronize()
-            t_cap.setdefault(k, []).append(drv.pcg_dev(rhs, x, 1e-300, k).ms)
-    slope_ms = (statistics.median(t_cap[k_hi]) - statistics.median(t_cap[k_lo])) / (k_hi - k_lo)
-    steady = {"method": f"slope of PCG solve time between {k_lo} and {k_hi} capped iterations "
-                        "(median of 3, CUDA events on the library stream)",
-              "ms_per_iteration": slope_ms,
-              "achieved_gbs": B_IT_VECTORS * 8.0 * N / (slope_ms * 1e-3) / 1e9,
-              "fixed_ms_per_solve": statistics.median(t_cap[k_lo]) - k_lo * slope_ms}
-    steady["frac"] = steady["achieved_gbs"] / peak
+    steady = _steady_state(drv, rhs, x, N, peak)
+
+    # ADMM step time at C2 (full outer iteration: build_rhs, PCG, B y,
+    # updates, residuals, dual_inf), continuing from the zero state
+    admm = None
+    if args.admm_steps > 0:
+        recs = [drv.step() for _ in range(args.admm_steps)]
+        sm = statistics.mean(r.step_ms for r in recs)
+        admm = {"steps": len(recs), "step_ms_mean": sm, "steps_per_s": 1e3 / sm,
+                "pcg_ms_mean": statistics.mean(r.pcg_ms for r in recs),
+                "inner_iters": [r.inner_iters for r in recs],
+                "r_eq_last": recs[-1].r_eq, "r_u_last": recs[-1].r_u,
+                "note": "C2 under the BASELINE mapping (delta = rho = 1) does not reach tol_primal "
+                        "1e-6 within 100k steps (DESIGN.md 9): its 'ADMM solve time' is reported per "
+                        "step; admm_solve.C0 is the full solve to convergence"}
+    del drv, pc, op, rhs, x
+
+    configs, admm_solve = {}, {}
+    if rank == 0 and world == 1 and args.configs:
+        for name in [n for n in args.configs.split(",") if n]:
+            try:
+                if name == "C0":
+                    admm_solve["C0"] = measure_c0_solve(ctx)
+                elif name == "C1":
+                    configs["C1"] = measure_c1(ctx, peak)
+                else:
+                    configs[name] = measure_config(name, ctx, peak, peak_kind)
+            except Exception as e:  # noqa: BLE001
+                configs[name] = {"error": f"{type(e).__name__}: {e}"}
+            torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             times, cores = reference_sample(args.cpu_iters, 1, shape)
             cpu = {"value": len(times) / sum(times), "unit": "it/s", "cores": cores,
-                   "kind": "reference",
-                   "sample": f"{len(times)} iterations of the unchanged reference pcg loop body "
-                             f"on the same C2 system (oracle/_ref, FFTW3 shim, {cores} threads)"}
+                   "kind": "reference", "sample": _ref_sample_text(len(times), shape, 1, cores),
+                   "fftw": _fftw_note()}
+            if args.cpu_iters_1t > 0:
+                t1, _ = reference_sample(args.cpu_iters_1t, 0, shape, threads=1)
+                cpu["one_thread"] = {"value": len(t1) / sum(t1), "unit": "it/s", "cores": 1,
+                                     "sample": _ref_sample_text(len(t1), shape, 0, 1)}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "it/s", "cores": _host_cores(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -358,13 +532,14 @@ def run_b200(args):
                 "ms_per_step": t_max / args.steps, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded std::mt19937_64 target state, BASELINE C2 formulas)",
-                "config": _config(shape, {"iters_per_step": iters / args.steps,
-                                          "pcg_ms_inside_api": pcg_ms / args.steps,
-                                          "x0": ("pre-zeroed device buffer per timed step (x is in/out)"
-                                                 if n_pre else "zeroed inside the timed step")}),
+                "config": _config(shape),
+                "step_detail": {"iters_per_step": iters / args.steps,
+                                "pcg_ms_inside_api": pcg_ms / args.steps,
+                                "x0": ("pre-zeroed device buffer per timed step (x is in/out)"
+                                       if n_pre else "zeroed inside the timed step")},
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roofline,
                 "iteration_roofline": iter_roof, "steady_state_iteration": steady,
-                "passes": passes, "admm": admm,
+                "passes": passes, "admm": admm, "admm_solve": admm_solve, "configs": configs,
                 "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     if dist:
@@ -381,7 +556,11 @@ def main():
     ap.add_argument("--shape", type=int, nargs=3, default=[256, 256, 256])
     ap.add_argument("--admm-steps", type=int, default=3)
     ap.add_argument("--profile-reps", type=int, default=10)
+    ap.add_argument("--configs", default="C0,C3,C4,C1",
+                    help="comma list of extra BASELINE configs measured after the headline "
+                         "(C0 = full ADMM solve; C1 = operator microbenchmark); '' for none")
     ap.add_argument("--cpu-iters", type=int, default=3)
+    ap.add_argument("--cpu-iters-1t", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def test_bench_json_contract():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3", "--warmup", "3",
                           "--no-cpu-baseline", "--admm-steps", "1", "--profile-reps", "2",
-                          "--shape", "32", "128", "128"], capture_output=True, text=True, timeout=600)
+                          "--shape", "32", "128", "128", "--configs", "C0"], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
     assert len(lines) == 1
@@ -34,3 +34,7 @@ def test_bench_json_contract():
     assert e["d2h_bytes_per_step"] == 8 * 32 * 128 * 128
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["steady_state_iteration"]["ms_per_iteration"] > 0
+    # the C0 full ADMM solve: the reference's step and Krylov counts
+    c0 = d["admm_solve"]["C0"]
+    assert c0["status"] == "converged" and c0["same_counts"], c0
+    assert r["traffic"] is None  # no ncu capture for this shape
