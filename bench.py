@@ -80,8 +80,8 @@ def _fftw_note():
         out = subprocess.run(["ldconfig", "-p"], capture_output=True, text=True, timeout=10).stdout
     except Exception:  # noqa: BLE001
         return "unknown (ldconfig failed)"
-    libs = sorted({ln.split()[0] for ln in out.splitlines() if "fftw3" in ln})
-    cpu = [x for x in libs if not x.startswith("libcufftw")]
+    libs = sorted({ln.split()[0] for ln in out.splitlines() if "fftw" in ln})
+    cpu = [x for x in libs if not x.startswith("libcufftw") and "fftw3" in x]
     if cpu:
         return "host has CPU FFTW3 (" + ", ".join(cpu) + "); the baseline still links the builder's shim"
     seen = ("ldconfig lists only " + ", ".join(libs) + ", cuFFT's FFTW-API wrapper (a GPU library)"

@@ -199,6 +199,15 @@ fdg_status fdg_admm_objective(fdg_admm adm, double* out);
  * Clobbers the PCG scratch vectors. */
 fdg_status fdg_admm_profile_passes(fdg_admm adm, int reps, double* ms, double* bytes);
 
+/* Size threshold of the graph-driven PCG iterations (no reference
+ * counterpart; a tuning knob of this library): solves with N <= nmax run
+ * their steady-state iterations inside one CUDA graph launch (a WHILE node
+ * over a two-iteration body, stopped by the device control step) instead of
+ * host-sequenced launches.  Same kernels, same order, same results.  nmax < 0
+ * leaves it unchanged; *previous (optional) receives the old value.
+ * Default 2^21, or the FDG_PCG_GRAPH_NMAX environment variable. */
+fdg_status fdg_set_pcg_graph_nmax(long long nmax, long long* previous);
+
 /* --------------------------------------------------- synthetic inputs */
 /* std::mt19937_64(seed) + std::normal_distribution<double> in layout order
  * (the reference tests' generator, test_toeplitz.cpp:15-20). */

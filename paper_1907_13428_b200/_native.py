@@ -99,6 +99,7 @@ _sig("fdg_admm_pcg_host", _st, _vp, _dp, _dp, C.c_double, C.c_int, C.POINTER(Pcg
 _sig("fdg_admm_dual_inf", _st, _vp, _dp)
 _sig("fdg_admm_objective", _st, _vp, _dp)
 _sig("fdg_admm_profile_passes", _st, _vp, C.c_int, _dp, _dp)
+_sig("fdg_set_pcg_graph_nmax", _st, C.c_longlong, C.POINTER(C.c_longlong))
 _sig("fdg_admm_debug_get", _st, _vp, C.c_int, _dp)
 
 PASS_NAMES = ["K1_row_p_update_B", "K2_col_S_mid", "K3_row_BT_update", "P1_hartley_x2",

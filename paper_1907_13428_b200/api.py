@@ -110,6 +110,14 @@ class Context:
 _default_ctx: Context | None = None
 
 
+def set_pcg_graph_nmax(nmax: int) -> int:
+    """Size threshold of the graph-driven PCG iterations (fdg_set_pcg_graph_nmax);
+    returns the previous value.  0 disables them."""
+    prev = C.c_longlong()
+    check(lib.fdg_set_pcg_graph_nmax(int(nmax), C.byref(prev)))
+    return int(prev.value)
+
+
 def default_context() -> Context:
     global _default_ctx
     if _default_ctx is None:

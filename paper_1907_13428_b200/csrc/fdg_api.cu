@@ -13,6 +13,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <functional>
@@ -303,6 +304,7 @@ enum Scal {
   S_OBJ = S_DINF + 2,   // 2
   S_DOT = S_OBJ + 2,
   S_ONE,  // constant 1.0 (alpha of the fused residual r = b - 1 * S x)
+  S_TOL,  // (tol |b|)^2 of the running solve (graph-driven iterations)
   S_COUNT
 };
 
@@ -567,6 +569,22 @@ struct fdg_admm_s {
   int* x0flag_host = nullptr;  // pinned
   double seq = 0.0;
   double hseq[2] = {0.0, 0.0};
+  // graph-driven PCG iterations (pcg_dev): instantiated graphs keyed by the
+  // solution buffer and the parity of their first iteration
+  struct PcgGraph {
+    const double* x = nullptr;
+    const double* rhs = nullptr;
+    int parity = 0;
+    cudaGraphExec_t exec = nullptr;
+    unsigned long long kernels = 0;  // launches per body execution
+    unsigned long long used = 0;
+  };
+  std::vector<PcgGraph> graphs;
+  unsigned long long graph_tick = 0;
+  ~fdg_admm_s() {
+    for (auto& g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+  }
 };
 
 namespace {
@@ -657,9 +675,36 @@ void wait_status(cudaStream_t st, const volatile double* hs, double seq) {
   std::atomic_thread_fence(std::memory_order_acquire);
 }
 
-#ifndef FDG_PCG_SPECULATE
-#define FDG_PCG_SPECULATE 0
+// Spin until the graph-driven iterations reported their stop (rep[3] = the
+// iteration number, written last).
+void wait_report(cudaStream_t st, const volatile double* rep) {
+  for (unsigned spin = 0;; ++spin) {
+    if (rep[3] != 0.0) break;
+    if ((spin & 1023u) == 1023u) {
+      const cudaError_t e = cudaStreamQuery(st);
+      if (e == cudaSuccess) {
+        if (rep[3] != 0.0) break;
+        fail(FDG_ECUDA, "pcg: graph stop report missing");
+      }
+      if (e != cudaErrorNotReady) ck(e, "graph status");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+}
+
+// Graph-driven PCG iterations for the latency-bound sizes: N up to
+// FDG_PCG_GRAPH_NMAX (env; default 2^21 elements, 0 disables) with the
+// standard preconditioner passes (the dense any-n path has no guards).
+#ifndef FDG_GRAPH_PDL
+#define FDG_GRAPH_PDL 0
 #endif
+std::atomic<long long> g_graph_nmax{[] {
+  const char* e = std::getenv("FDG_PCG_GRAPH_NMAX");
+  return e ? std::atoll(e) : (1LL << 21);
+}()};
+bool graph_enabled(const fdg_admm_s* a, size_t N) {
+  return (long long)N <= g_graph_nmax.load() && !a->pc->dense && !a->pc->pipe.p;
+}
 
 // pcg (admm.cpp:121-169) with apply = apply_S, precond = pc.solve.
 // on_final_x (optional): called right after the x update that precedes a
@@ -739,45 +784,116 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
       ck(fdg::launch_axpy_dev(st, lc, x, dir_cur(it), N, sc.at(slot_cur(it)), sc.at(S_PQ)), "x += a p");
       x_host = it;
     };
-    auto enqueue = [&](int it, bool guarded) {
+    // graph: launch the control step of the graph-driven iterations
+    // (k_pcg_control_graph, condition handle `cond`) instead of the
+    // host-sequenced one
+    auto enqueue_g = [&](int it, bool guarded, bool graph, cudaGraphConditionalHandle cond) {
       const int* g = guarded ? pause : nullptr;
       const int cur = slot_cur(it), prv = slot_prv(it);
-      const bool upd = it > 1 && x_host != it - 1;  // alpha_{it-1} = rz(prv) / pq (S_PQ still holds pq_{it-1})
+      const bool upd = graph || (it > 1 && x_host != it - 1);  // alpha_{it-1} = rz(prv) / pq (S_PQ still holds pq_{it-1})
+      const bool first = !graph && it == 1;
       ck(fdg::launch_row_fused(st, lc, a->z.d(), dir_prv(it), dir_cur(it), x, a->u.d(), op->nt, op->n1, op->n2,
                                op->row_axis(), op->scale2(), tf, op->psi, sc.at(prv), sc.at(S_PQ), sc.at(cur),
-                               sc.at(prv), it == 1, upd, g),
+                               sc.at(prv), first, upd, g),
          "K1F row");
       ck(fdg::launch_col_s_mid(st, lc, dir_cur(it), a->u.d(), a->w.d(), a->vp.d(), op->nt, op->n1, op->n2, op->ax1,
                                op->scale1(), a->inv_m2.d(), a->a1.d(), sc.slot(S_PQ), g),
          "K2 col");
       ck(fdg::launch_row_s_out(st, lc, a->w.d(), a->vp.d(), nullptr, a->r.d(), op->nt, op->n1, op->n2,
                                op->row_axis(), op->scale2(), tf, op->psi, sc.at(cur), sc.at(S_PQ), sc.slot(S_RR), g,
-                               it == 1 && r_is_b ? rhs : nullptr),
+                               first && r_is_b ? rhs : nullptr),
          "K3 row");
-      a->seq += 1.0;
-      a->hseq[it & 1] = a->seq;
-      ck(fdg::launch_pcg_control(st, lc, sc.at(S_PQ), sc.at(S_RR), (tol * nb) * (tol * nb),
-                                 a->hstat_dev + 4 * (it & 1), pause, g, a->seq),
-         "control");
+      if (graph) {
+        ck(fdg::launch_pcg_control_graph(st, lc, sc.at(S_PQ), sc.at(S_RR), sc.at(S_TOL), a->hstat_dev, pause,
+                                         static_cast<int*>(a->ctl.p), cond),
+           "control (graph)");
+      } else {
+        a->seq += 1.0;
+        a->hseq[it & 1] = a->seq;
+        ck(fdg::launch_pcg_control(st, lc, sc.at(S_PQ), sc.at(S_RR), (tol * nb) * (tol * nb),
+                                   a->hstat_dev + 4 * (it & 1), pause, g, a->seq),
+           "control");
+      }
       pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(prv), pause);  // r.z' -> prv slot
     };
+    auto enqueue = [&](int it, bool guarded) { enqueue_g(it, guarded, false, 0); };
+    // Graph-driven iterations (latency-bound sizes, FDG_PCG_GRAPH_NMAX): the
+    // steady-state iterations (guarded, x update carried in K1F) of one solve
+    // run inside ONE graph launch whose WHILE node repeats a two-iteration
+    // body (parities fixed by the first iteration) until the control step
+    // stops it; the host then handles the stop exactly like a paused
+    // host-sequenced iteration.  Graphs are cached per (x, rhs, parity).
+    const bool use_graph = graph_enabled(a, N);
+    auto graph_for = [&](int parity) -> fdg_admm_s::PcgGraph& {
+      for (auto& g : a->graphs)
+        if (g.x == x && g.rhs == rhs && g.parity == parity) {
+          g.used = ++a->graph_tick;
+          return g;
+        }
+      if (a->graphs.size() >= 8) {  // evict the least recently used
+        auto it = std::min_element(a->graphs.begin(), a->graphs.end(),
+                                   [](const auto& p, const auto& q) { return p.used < q.used; });
+        if (it->exec) cudaGraphExecDestroy(it->exec);
+        a->graphs.erase(it);
+      }
+      fdg_admm_s::PcgGraph gr;
+      gr.x = x;
+      gr.rhs = rhs;
+      gr.parity = parity;
+      cudaGraph_t graph = nullptr;
+      ck(cudaGraphCreate(&graph, 0), "graph create");
+      cudaGraphConditionalHandle cond;
+      ck(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault), "graph cond");
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = cond;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t node;
+      ck(cudaGraphAddNode(&node, graph, nullptr, 0, &cp), "graph while node");
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      const unsigned long long l0 = lc->count;
+      const int x_host_saved = x_host;
+      fdg::pdl_suspend(!FDG_GRAPH_PDL);
+      ck(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal),
+         "graph capture");
+      enqueue_g(2 + parity, true, true, cond);  // parity of the first body iteration
+      enqueue_g(3 + parity, true, true, cond);
+      cudaGraph_t captured = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(st, &captured);
+      fdg::pdl_suspend(false);
+      ck(ec, "graph end capture");
+      x_host = x_host_saved;
+      gr.kernels = lc->count - l0;
+      lc->count = l0;  // counted per executed body instead
+      ck(cudaGraphInstantiate(&gr.exec, graph, 0), "graph instantiate");
+      cudaGraphDestroy(graph);
+      gr.used = ++a->graph_tick;
+      a->graphs.push_back(gr);
+      return a->graphs.back();
+    };
     if (!r_is_b) pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(slot_cur(1)));
-    if (max_inner >= 1) enqueue(1, true);
-    for (int it = 1; it <= max_inner; ++it) {
-      // FDG_PCG_SPECULATE: enqueue iteration it+1 before reading iteration
-      // it's status.  Off by default: the host reads the status right after
-      // the control step and enqueues it+1 while the GPU still runs the ~0.3
-      // ms preconditioner of it, so nothing is lost, and at convergence no
-      // speculative iteration has to drain through its guards.
-      if (FDG_PCG_SPECULATE && it < max_inner) enqueue(it + 1, true);
-      const volatile double* hs = a->hstat + 4 * (it & 1);
-      wait_status(st, hs, a->hseq[it & 1]);
-      const double pq = hs[0];
-      double rn = std::sqrt(hs[1]);
-      if (hs[2] != 0.0) {
-        // iteration it paused the stream: the speculative launches behind it
-        // exit at their guard; the flag is cleared in stream order after
-        // them (no host drain: the confirmation below queues right behind)
+    int it = 1;
+    double pq = 0.0, rr2 = 0.0;
+    bool stop = false;
+    auto read_status = [&](int i) {  // the host-sequenced iteration i
+      const volatile double* hs = a->hstat + 4 * (i & 1);
+      wait_status(st, hs, a->hseq[i & 1]);
+      pq = hs[0];
+      rr2 = hs[1];
+      stop = hs[2] != 0.0;
+    };
+    if (max_inner >= 1) {
+      enqueue(1, true);
+      read_status(1);
+    }
+    bool cap = max_inner < 1;
+    while (!cap) {
+      double rn = std::sqrt(rr2);
+      if (stop) {
+        // iteration it paused the stream: the launches behind it exit at
+        // their guard; the flag is cleared in stream order after them (no
+        // host drain: the work below queues right behind)
         ck(cudaMemsetAsync(pause, 0, sizeof(int), st), "clear pause");
         if (!std::isfinite(pq) || pq <= 0.0)
           fail(FDG_ENUMERIC, "pcg: operator lost positive definiteness", FDG_NUM_PD_LOSS);
@@ -788,9 +904,9 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
           x_update(it);
           if (on_final_x) on_final_x();
           apply_S_dev(a, x, nullptr, a->r.d(), rhs, sc.slot(S_RR2));
-          double rr2;
-          sc.read(S_RR2, 1, &rr2);
-          rn = std::sqrt(rr2);
+          double rr;
+          sc.read(S_RR2, 1, &rr);
+          rn = std::sqrt(rr);
           if (rn <= tol * nb) {
             res = {it, 1, rn / nb, 0.0};
             finish();
@@ -799,10 +915,35 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
         }
         // continue (from the replaced residual): the skipped tail of it, then it+1
         pc_apply_dev(a->pc, a->r.d(), a->z.d(), a->u.d(), a->r.d(), sc.slot(slot_prv(it)));
-        if (it < max_inner) enqueue(it + 1, true);
-      } else if (!FDG_PCG_SPECULATE && it < max_inner) {
-        enqueue(it + 1, true);
+        if (it >= max_inner) break;
+        ++it;
+        enqueue(it, true);  // x update of it-1 done by the host: not a graph iteration
+        read_status(it);
+        continue;
       }
+      if (it >= max_inner) break;
+      if (use_graph) {
+        // iterations it+1.. on the device until the control step stops
+        auto& gr = graph_for((it + 1) & 1);
+        a->hstat[11] = 0.0;
+        ck(fdg::launch_pcg_graph_prep(st, lc, static_cast<int*>(a->ctl.p), it, max_inner, sc.at(S_TOL),
+                                      (tol * nb) * (tol * nb)),
+           "graph prep");
+        ck(cudaGraphLaunch(gr.exec, st), "graph launch");
+        const volatile double* rep = a->hstat + 8;
+        wait_report(st, rep);
+        const int it_end = (int)rep[3];
+        pq = rep[0];
+        rr2 = rep[1];
+        stop = rep[2] != 0.0;
+        lc->count += gr.kernels * (unsigned long long)((it_end - it + 1) / 2);  // body executions
+        if (!stop) ck(cudaMemsetAsync(pause, 0, sizeof(int), st), "clear pause");  // the cap raised it
+        it = it_end;
+        continue;
+      }
+      ++it;
+      enqueue(it, true);
+      read_status(it);
     }
     if (max_inner >= 1 && x_host != max_inner) x_update(max_inner);  // no K1F carries the last update
     ck(cudaStreamSynchronize(st), "drain");
@@ -1388,8 +1529,8 @@ fdg_status fdg_admm_create(fdg_op op, fdg_pc pc, const fdg_admm_desc* desc, cons
     ck(cudaEventCreateWithFlags(&a->ev_norms, cudaEventDisableTiming), "event");
     a->ctl.alloc(sizeof(int) * 4);
     ck(cudaMemsetAsync(a->ctl.p, 0, sizeof(int) * 4, st), "memset");
-    ck(cudaHostAlloc(&a->hstat, sizeof(double) * 8, cudaHostAllocMapped), "pinned status");
-    for (int i = 0; i < 8; ++i) a->hstat[i] = -1.0;
+    ck(cudaHostAlloc(&a->hstat, sizeof(double) * 12, cudaHostAllocMapped), "pinned status");
+    for (int i = 0; i < 12; ++i) a->hstat[i] = i < 8 ? -1.0 : 0.0;
     ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a->hstat_dev), a->hstat, 0), "mapped status");
     ck(cudaStreamSynchronize(st), "sync");
     *out = a.release();
@@ -1592,6 +1733,13 @@ fdg_status fdg_admm_objective(fdg_admm a, double* out) {
 // events on the context stream.  Overwrites the PCG scratch vectors (run it
 // after the measurements that need them).  Order of ms[]: K1 row, K2 col,
 // K3 row, P1 x2, P2 x1, P3 t, P4 x1, P5 x2 (K1 = fused CG update + B row).
+fdg_status fdg_set_pcg_graph_nmax(long long nmax, long long* previous) {
+  return guard([&] {
+    const long long old = nmax >= 0 ? g_graph_nmax.exchange(nmax) : g_graph_nmax.load();
+    if (previous) *previous = old;
+  });
+}
+
 fdg_status fdg_admm_profile_passes(fdg_admm a, int reps, double* ms, double* bytes) {
   return guard([&] {
     if (!a || reps < 1) fail(FDG_EINVAL, "fdg_admm_profile_passes: bad arguments");

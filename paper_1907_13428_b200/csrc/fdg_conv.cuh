@@ -535,6 +535,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
   pdl_wait();
   if (paused(a.guard)) return;
   constexpr int TILE = CP::TILE;
+  constexpr bool DB = MODE == 2;  // double-buffered staging
   const CMap<L, LY == 1, Cf::HOMO_COL> mp;
   const int g = mp.g, b = mp.b, t = mp.t;
   const int n = a.n, C = a.C;
@@ -555,7 +556,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
   __syncthreads();  // tables
   double e = 0.0;
   int buf = 0;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= (MODE == 2)) {
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= DB) {
     const int o = tile / ncb;
     const long c = (long)((tile - o * ncb) * G + g) * 2;
     const bool vc = PF || c < C;
@@ -572,7 +573,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
       for (int m = 0; m < R; ++m) v[m] = *reinterpret_cast<const double2*>(st_in + (t + m * T) * P + 2 * g);
       if constexpr (MODE != 2) __syncthreads();  // single input buffer
       if (nxt < ntiles) {
-        FDG_IO(stage_tile(S.stage + (buf ^ (MODE == 2)) * TILE, a.x, nxt));
+        FDG_IO(stage_tile(S.stage + (buf ^ DB) * TILE, a.x, nxt));
         if constexpr (MODE == 2) FDG_IO(stage_tile(S.stage + (2 + (buf ^ 1)) * TILE, a.acc, nxt));
       }
       cp_async_commit();
@@ -629,6 +630,11 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
       const int id0 = mp.half_id(0), id1 = mp.half_id(1);
 #pragma unroll
       for (int m = 0; m < R; ++m) v[m] = sm[slot<LY, M, G2>(t + T * m, m < HR ? id0 : id1)];
+      // write-after-read across the halves: each half reads the other's
+      // slots above, and the first scatter of its transform below is guarded
+      // only by its own half barrier (lane_sync), so a lagging half could
+      // still be reading the slots the other half overwrites
+      pair_sync<L, LY, Cf::HOMO_COL>();
       conv_half<L, LY>(v, S.ex, t, mp.gs, b, S.tw, S.twist, S.sym);
       conv_combine<L, LY, !PF>(v, y, S.ex, mp, S.twist);
 #pragma unroll

@@ -117,6 +117,20 @@ cudaError_t launch_pc_pipe(cudaStream_t st, LaunchCounter* lc, const double* in,
 // (pq <= 0 / non-finite, non-finite residual, or |r| <= tol |b|).
 cudaError_t launch_pcg_control(cudaStream_t st, LaunchCounter* lc, const double* pq, const double* rr,
                                double tol_nb2, double* out, int* pause, const int* guard, double seq);
+// Control step of the graph-driven PCG iterations (a CUDA graph whose WHILE
+// node repeats a two-iteration body): ctl[1] counts iterations, ctl[2] is
+// max_inner, *tol_nb2 the stop threshold (tol |b|)^2 of this solve.  Writes
+// (pq, |r|^2, stop) of every iteration into out[4 (it & 1) ..]; when it stops
+// (breakdown, |r| small, or the cap) it raises the pause flag, clears the
+// WHILE condition and reports (pq, |r|^2, stop, it) in out[8..11], it last.
+cudaError_t launch_pcg_control_graph(cudaStream_t st, LaunchCounter* lc, const double* pq, const double* rr,
+                                     const double* tol_nb2, double* out, int* pause, int* ctl,
+                                     cudaGraphConditionalHandle cond);
+// PDL launch attributes off while this thread captures a graph body
+void pdl_suspend(bool on);
+// ctl[1] = it0 - 1, ctl[2] = max_inner, *tol_slot = tol_nb2 (stream ordered)
+cudaError_t launch_pcg_graph_prep(cudaStream_t st, LaunchCounter* lc, int* ctl, int it0m1, int max_inner,
+                                  double* tol_slot, double tol_nb2);
 
 // ------------------------------------------------------------- elementwise
 cudaError_t launch_copy(cudaStream_t st, LaunchCounter* lc, double* dst, const double* src, size_t N);

@@ -493,6 +493,63 @@ cudaError_t launch_pcg_control(cudaStream_t st, LaunchCounter* lc, const double*
   return pdl_launch(PDL_MISC, k_pcg_control, 1, 1, 0, st, pq, rr, tol_nb2, out, pause, guard, seq);
 }
 
+__global__ void k_pcg_control_graph(const double* pq, const double* rr, const double* tol_nb2, double* out,
+                                    int* pause, int* ctl, cudaGraphConditionalHandle cond) {
+  pdl_trigger();
+  pdl_wait();
+  volatile int* vctl = ctl;
+  if (*reinterpret_cast<volatile int*>(pause)) {  // an earlier iteration of this body stopped
+    cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  const int it = vctl[1] + 1;
+  vctl[1] = it;
+  const double p = *pq, r2 = *rr;
+  const bool bad = !isfinite(p) || p <= 0.0 || !isfinite(r2);
+  // slightly looser than the host's |r| <= tol |b| (see k_pcg_control)
+  const bool stop = bad || r2 <= *tol_nb2 * (1.0 + 1e-12);
+  volatile double* o = out + 4 * (it & 1);
+  o[0] = p;
+  o[1] = r2;
+  o[2] = stop ? 1.0 : 0.0;
+  if (stop || it >= vctl[2]) {
+    *reinterpret_cast<volatile int*>(pause) = 1;  // the rest of the body exits at its guards
+    cudaGraphSetConditional(cond, 0);
+    volatile double* rep = out + 8;
+    rep[0] = p;
+    rep[1] = r2;
+    rep[2] = stop ? 1.0 : 0.0;
+    __threadfence_system();
+    rep[3] = (double)it;
+  }
+}
+
+__global__ void k_pcg_graph_prep(int* ctl, int it0m1, int max_inner, double* tol_slot, double tol_nb2) {
+  ctl[1] = it0m1;
+  ctl[2] = max_inner;
+  *tol_slot = tol_nb2;
+}
+
+cudaError_t launch_pcg_control_graph(cudaStream_t st, LaunchCounter* lc, const double* pq, const double* rr,
+                                     const double* tol_nb2, double* out, int* pause, int* ctl,
+                                     cudaGraphConditionalHandle cond) {
+  count(lc);
+  return pdl_launch(PDL_MISC, k_pcg_control_graph, 1, 1, 0, st, pq, rr, tol_nb2, out, pause, ctl, cond);
+}
+
+cudaError_t launch_pcg_graph_prep(cudaStream_t st, LaunchCounter* lc, int* ctl, int it0m1, int max_inner,
+                                  double* tol_slot, double tol_nb2) {
+  count(lc);
+  k_pcg_graph_prep<<<1, 1, 0, st>>>(ctl, it0m1, max_inner, tol_slot, tol_nb2);
+  return cudaGetLastError();
+}
+
+namespace {
+thread_local bool t_pdl_off = false;
+}
+bool pdl_suspended() { return t_pdl_off; }
+void pdl_suspend(bool on) { t_pdl_off = on; }
+
 bool pdl_after(bool l1) {
   thread_local bool last_l1 = false;
   const bool ok = !l1 || last_l1;

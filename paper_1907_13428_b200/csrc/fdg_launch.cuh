@@ -93,6 +93,8 @@ inline void count(LaunchCounter* lc, unsigned long long k = 1) {
 enum PdlClass { PDL_KROW = 1, PDL_KCOL = 2, PDL_PROW = 4, PDL_PCOL = 8, PDL_TF = 16, PDL_MISC = 32, PDL_L1 = 64 };
 int pdl_mask();             // fdg_kernels.cu: FDG_PDL_MASK (env) or the default
 bool pdl_after(bool l1);    // fdg_kernels.cu: whether PDL may be used, records this launch
+bool pdl_suspended();       // fdg_kernels.cu: PDL off while this thread captures a graph body
+void pdl_suspend(bool on);
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t pdl_launch(int cls, void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem,
@@ -107,7 +109,7 @@ inline cudaError_t pdl_launch(int cls, void (*kernel)(KArgs...), unsigned grid, 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   const bool after = pdl_after((cls & PDL_L1) != 0);
-  cfg.numAttrs = (FDG_PDL && (pdl_mask() & cls & 63) && after) ? 1 : 0;
+  cfg.numAttrs = (FDG_PDL && (pdl_mask() & cls & 63) && after && !pdl_suspended()) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 

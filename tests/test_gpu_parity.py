@@ -211,7 +211,10 @@ def test_admm_five_steps_golden(gpu_ctx, ref, golden, n):
                                    # k_colc<512|1024|2048, 2> the bench times (K2) and the
                                    # staged row passes k_rowc<512> / k_rowq<1024> / k_rowc<2048>
                                    (2, 256, 256), (2, 512, 64), (2, 1024, 32), (2, 16, 1024),
-                                   (2, 512, 512)])
+                                   (2, 512, 512),
+                                   # more tiles than resident CTAs: the persistent loops'
+                                   # staging / prefetch across tiles
+                                   (24, 256, 256), (8, 512, 256)])
 def test_pcg_noncube_vs_port(gpu_ctx, port, shape):
     """PCG on the ADMM normal equations for shapes that select the staged
     row kernels (tiles inside one slice), the L >= 1024 single-buffer
@@ -272,3 +275,43 @@ def test_pcg_host_x0_paths(gpu_ctx, ref, golden, x0_kind):
     torch.cuda.synchronize()
     assert r_host.iterations == r_dev.iterations
     assert np.array_equal(xh, x_d.cpu().numpy())
+
+
+@pytest.mark.parametrize("shape", [(32, 32, 32), (8, 16, 64), (5, 12, 16)])
+def test_pcg_graph_iterations_match_host_sequenced(gpu_ctx, shape):
+    """The graph-driven PCG iterations (one CUDA graph launch per solve, a
+    WHILE node stopped by the device control step) run the same kernels in
+    the same order as the host-sequenced loop: identical Krylov counts and
+    bitwise-identical solutions, for converged solves, the max_inner cap
+    (both parities of the stopping iteration) and whole ADMM steps."""
+    import torch
+    from paper_1907_13428_b200 import make_problem
+    from paper_1907_13428_b200.api import set_pcg_graph_nmax
+    out = {}
+    prev = set_pcg_graph_nmax(0)
+    try:
+        for mode, nmax in (("host", 0), ("graph", 1 << 40)):
+            set_pcg_graph_nmax(nmax)
+            c, op, pc, drv = make_problem("C0", shape, ctx=gpu_ctx)
+            rhs, _ = drv.build_rhs()
+            rhs_d = torch.tensor(rhs, device="cuda")
+            runs = []
+            for tol, cap in ((1e-8, 400), (1e-30, 5), (1e-30, 6), (1e-30, 1)):
+                x = torch.zeros_like(rhs_d)
+                torch.cuda.synchronize()
+                r = drv.pcg_dev(rhs_d, x, tol, cap)
+                torch.cuda.synchronize()
+                runs.append((r.iterations, r.converged, r.rel_residual, x.cpu().numpy()))
+            recs = [drv.step() for _ in range(4)]
+            runs.append([(s.inner_iters, s.r_eq, s.r_y, s.r_u, s.dual_inf) for s in recs])
+            runs.append(drv.get("y"))
+            out[mode] = runs
+    finally:
+        set_pcg_graph_nmax(prev)
+    h, g = out["host"], out["graph"]
+    for a, b in zip(h[:4], g[:4]):
+        assert a[:3] == b[:3]
+        assert np.array_equal(a[3], b[3])
+    assert h[0][0] > 4 and h[1][0] == 5 and h[2][0] == 6
+    assert h[4] == g[4]
+    assert np.array_equal(h[5], g[5])
