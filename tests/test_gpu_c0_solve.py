@@ -3,9 +3,11 @@ history (tests/golden/ref_c0_solve.*, the unchanged reference run to
 convergence on CPU: 11368 ADMM steps, 148204 Krylov iterations).
 
 Gates (BASELINE north_star): identical ADMM iteration count, Krylov
-iterations +-1 per step, final objective within 1e-8 relative; final
-residuals compared at 1e-8 relative to the magnitude of the terms they are
-differences of (they are ~1e-9 differences of O(1) quantities)."""
+iterations +-1 per step, final objective, y and v within 1e-8 relative; the
+final residuals r_eq, r_u, dual_inf within 1e-8 relative, or 4x the measured
+cross-implementation noise floor where that floor is above 1e-8
+(tests/golden/np_c0_solve.json, made by tests/golden/make_noise_floor.py:
+two CPU implementations with different FFT backends, same inputs); r_y == 0."""
 import json
 import os
 
@@ -46,5 +48,17 @@ def test_c0_full_solve_matches_reference(gpu_ctx):
     assert np.linalg.norm(y - g["y"]) <= 1e-8 * np.linalg.norm(g["y"])
     assert np.linalg.norm(v - g["v"]) <= 1e-8 * np.linalg.norm(g["v"])
     r_eq, r_y, r_u, dinf = res[-1]
-    assert abs(r_u - ref["r_u"]) <= 1e-8 * np.abs(g["v"]).max() / c["psi"]
-    assert abs(r_eq - ref["r_eq"]) <= 1e-8 * np.abs(g["v"]).max()
+    got = dict(r_eq=r_eq, r_y=r_y, r_u=r_u, dual_inf=dinf)
+    rd = {k: abs(got[k] - ref[k]) / abs(ref[k]) if ref[k] else abs(got[k]) for k in got}
+    print("final residuals gpu vs reference (relative):", {k: f"{v:.2e}" for k, v in rd.items()})
+    # Gates: 1e-8 relative (north_star) or, where that is below the measured
+    # cross-implementation noise floor (tests/golden/np_c0_solve.json: the
+    # numpy/pocketfft restatement vs the reference on the same inputs), 4x
+    # that floor.  r_eq and r_u are infinity norms of residuals ~1e-6 below
+    # the terms they are differences of, so a relative perturbation eps of
+    # the iterates moves them by ~1e6 eps.
+    floor = json.load(open(os.path.join(HERE, "golden", "np_c0_solve.json")))["rel_diff_vs_ref"]
+    for k in ("r_eq", "r_u", "dual_inf"):
+        tol = max(1e-8, 4.0 * floor.get(k, 0.0))
+        assert rd[k] <= tol, (k, rd[k], tol)
+    assert got["r_y"] == ref["r_y"] == 0.0  # no state box at C0: z_y = y
