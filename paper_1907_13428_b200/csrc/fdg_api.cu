@@ -854,7 +854,11 @@ fdg_pcg_result pcg_dev(fdg_admm_s* a, const double* rhs, double* x, double tol, 
       cudaGraph_t body = cp.conditional.phGraph_out[0];
       const unsigned long long l0 = lc->count;
       const int x_host_saved = x_host;
-      fdg::pdl_suspend(!FDG_GRAPH_PDL);
+      static const bool graph_pdl = [] {
+        const char* e = std::getenv("FDG_GRAPH_PDL");
+        return e ? std::atoi(e) != 0 : FDG_GRAPH_PDL != 0;
+      }();
+      fdg::pdl_suspend(!graph_pdl);
       ck(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal),
          "graph capture");
       enqueue_g(2 + parity, true, true, cond);  // parity of the first body iteration
