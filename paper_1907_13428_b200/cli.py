@@ -149,13 +149,25 @@ def sweep_points(cfg: RunConfig):
     return pts
 
 
-def _run_point(p: RunConfig):
-    """fdeopt_main.cpp:159-175: (row, code); any failure -> a 'failed' row."""
+def _run_point(p: RunConfig, ctx=None):
+    """fdeopt_main.cpp:159-175: (row, code); any failure -> a 'failed' row.
+    ctx: the rank's device context (None: the default context, device 0)."""
     try:
-        res = solve_spec(p.spec, p.admm)
+        res = solve_spec(p.spec, p.admm, ctx=ctx)
         return fio.make_summary_row(p, p.admm.delta, res), (EXIT_OK if res["status"] == "converged" else EXIT_ITERCAP)
     except Exception:  # noqa: BLE001
         return fio.make_summary_row(p, p.admm.delta, {"status": "failed"}), EXIT_USAGE
+
+
+def _rank_context(local: int):
+    """The device context of this rank's solves (GPU LOCAL_RANK), or None
+    without CUDA (the CPU gloo tests stub the solve)."""
+    import torch
+    if not torch.cuda.is_available():
+        return None
+    torch.cuda.set_device(local)
+    from .api import Context
+    return Context(local)
 
 
 def cmd_sweep(args) -> int:
@@ -171,13 +183,12 @@ def cmd_sweep(args) -> int:
         import torch.distributed as dist
         from .replicas import gather_records, shard
         local = int(os.environ.get("LOCAL_RANK", "0"))
-        if torch.cuda.is_available():
-            torch.cuda.set_device(local)
+        ctx = _rank_context(local)  # every point of this rank solves on its own GPU
         own_group = not dist.is_initialized()
         if own_group:
             dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
         mine = shard(list(enumerate(pts)), rank, world)
-        done = [(i, *_run_point(p)) for i, p in mine]
+        done = [(i, *_run_point(p, ctx)) for i, p in mine]
         allrec = gather_records([(i, vars(r), c) for i, r, c in done], dist)
         if own_group:
             dist.destroy_process_group()

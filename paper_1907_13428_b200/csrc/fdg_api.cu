@@ -696,7 +696,7 @@ void wait_report(cudaStream_t st, const volatile double* rep) {
 // FDG_PCG_GRAPH_NMAX (env; default 2^21 elements, 0 disables) with the
 // standard preconditioner passes (the dense any-n path has no guards).
 #ifndef FDG_GRAPH_PDL
-#define FDG_GRAPH_PDL 0
+#define FDG_GRAPH_PDL 1
 #endif
 std::atomic<long long> g_graph_nmax{[] {
   const char* e = std::getenv("FDG_PCG_GRAPH_NMAX");

@@ -60,11 +60,14 @@ def _sweep_worker(rank, world, port, cfg_path, out):
     from paper_1907_13428_b200 import cli
     from paper_1907_13428_b200 import io as fio
 
-    def fake_point(p):
+    def fake_point(p, ctx=None):
+        # every point of a rank is solved on that rank's own device context
+        assert ctx == ("ctx", rank), ctx
         res = {"status": "converged" if p.admm.delta < 1.0 else "itercap", "iterations": int(10 * p.admm.delta),
                "pcg_avg": float(rank), "misfit": 0.5, "dual_inf": 1e-9, "wall_seconds": 0.0}
         return fio.make_summary_row(p, p.admm.delta, res), (0 if res["status"] == "converged" else 2)
     cli._run_point = fake_point
+    cli._rank_context = lambda local: ("ctx", local)
     buf = _io.StringIO()
     with contextlib.redirect_stdout(buf):
         rc = cli.main(["sweep", "--config", cfg_path])
