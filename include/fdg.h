@@ -193,9 +193,7 @@ fdg_status fdg_admm_objective(fdg_admm adm, double* out);
  * bytes.  9 entries: K1 row (direction update p = z + b p fused with
  * the B row pass), K2 x1 col (S mid), K3 row (B^T + r update), P1 x2
  * Hartley, P2 x1 Hartley, P3 t filter, P4 x1 Hartley, P5 x2 Hartley (+ r.z),
- * X x += a p (once per solve; per iteration it rides in K1).  When the
- * spatial pairs run fused through L2 (n1 == n2 in {256, 512}) P1 is the
- * x2+x1 kernel, P5 the x1+x2 + r.z kernel, and P2 / P4 report 0.
+ * X x += a p (once per solve; per iteration it rides in K1).
  * Clobbers the PCG scratch vectors. */
 fdg_status fdg_admm_profile_passes(fdg_admm adm, int reps, double* ms, double* bytes);
 

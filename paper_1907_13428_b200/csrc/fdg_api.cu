@@ -443,7 +443,6 @@ struct fdg_pc_s {
   // (fdg_kernels.cu k_cas_axis), cas tables and an N-double scratch vector
   bool dense = false;
   DevBuf cas_t, cas_1, cas_2, dtmp;
-  DevBuf pipe;  // nt + 1 counters of the fused axis-pair kernels (null: separate passes)
   PcTables tab;
   // kind 2 (Bluestein passes, fdg_kernels.cu k_bs_*): chirps, real eigenvalues,
   // chirp convolution axes and two work buffers
@@ -510,16 +509,6 @@ void pc_apply_dev(fdg_pc_s* pc, const double* r, double* z, double* h, const dou
     ck(fdg::launch_cas_axis(st, lc, h, tmp, nt, n1, n2, pc->cas_1.d()), "pc x1 inv");
     ck(fdg::launch_cas_axis(st, lc, tmp, z, (long)nt * n1, n2, 1, pc->cas_2.d()), "pc x2 inv");
     if (rdot) ck(fdg::launch_dot(st, lc, rdot, z, pc->N(), red), "pc r.z");
-    return;
-  }
-  if (pc->pipe.p) {
-    // x2+x1 and x1+x2 pairs fused through L2 (fdg_pcfused.cuh); h != z here
-    int* ready = static_cast<int*>(pc->pipe.p);
-    ck(fdg::launch_pc_pipe(st, lc, r, h, h, nullptr, none, pc->nt, pc->n1, pc->tab.tw_1, ready, true, guard),
-       "pc x2+x1 fwd");
-    ck(fdg::launch_t_filter(st, lc, h, pc->tab, guard), "pc t filter");
-    ck(fdg::launch_pc_pipe(st, lc, h, h, z, rdot, red, pc->nt, pc->n1, pc->tab.tw_1, ready, false, guard),
-       "pc x1+x2 inv");
     return;
   }
   ck(fdg::launch_hartley_row(st, lc, r, h, F, pc->n2, pc->tab.tw_2, nullptr, none, guard), "pc x2 fwd");
@@ -703,7 +692,7 @@ std::atomic<long long> g_graph_nmax{[] {
   return e ? std::atoll(e) : (1LL << 21);
 }()};
 bool graph_enabled(const fdg_admm_s* a, size_t N) {
-  return (long long)N <= g_graph_nmax.load() && !a->pc->dense && !a->pc->pipe.p;
+  return (long long)N <= g_graph_nmax.load() && !a->pc->dense;
 }
 
 // pcg (admm.cpp:121-169) with apply = apply_S, precond = pc.solve.
@@ -1301,11 +1290,6 @@ fdg_pc_s* make_pc(fdg_ctx ctx, int nt, int n1, int n2, const double* lt, const d
   t.base = rho * (1.0 + 1.0 / delta);
   t.inv_m2 = 1.0 / m2;
   t.inv_total = 1.0 / (double)pc->N();
-  if (!dense && fdg::pc_pipe_supported(n1, n2)) {
-    pc->pipe.alloc(sizeof(int) * ((size_t)nt + 1));
-    ck(cudaMemsetAsync(pc->pipe.p, 0, sizeof(int) * ((size_t)nt + 1), st), "memset");
-    ck(cudaStreamSynchronize(st), "sync");
-  }
   ctx->ensure_partials(fdg::max_partials_needed(nt, n1, n2));
   return pc.release();
 }
@@ -1759,8 +1743,6 @@ fdg_status fdg_admm_profile_passes(fdg_admm a, int reps, double* ms, double* byt
     TimeFactor none_tf;
     const TimeFactor& stf = tf.kind == 1 ? tf : none_tf;
     Scalars& sc = a->sc;
-    const bool pipe = pc->pipe.p != nullptr;
-    int* ready = static_cast<int*>(pc->pipe.p);
     // well-defined scalars for the passes that read them
     const double one = 1.0;
     for (int s : {S_RZ0, S_RZ1, S_PQ})
@@ -1783,27 +1765,13 @@ fdg_status fdg_admm_profile_passes(fdg_admm a, int reps, double* ms, double* byt
         [&] { ck(fdg::launch_row_s_out(st, lc, a->w.d(), a->vp.d(), nullptr, a->r.d(), op->nt, op->n1, op->n2,
                                        op->row_axis(), op->scale2(), stf, op->psi, sc.at(S_RZ0), sc.at(S_PQ),
                                        sc.slot(S_DOT)), "K3"); },
-        [&] {
-          if (pipe)
-            ck(fdg::launch_pc_pipe(st, lc, a->r.d(), a->u.d(), a->u.d(), nullptr, RedSlot{}, pc->nt, pc->n1,
-                                   pc->tab.tw_1, ready, true),
-               "P12");
-          else
-            ck(fdg::launch_hartley_row(st, lc, a->r.d(), a->u.d(), F, pc->n2, pc->tab.tw_2, nullptr, RedSlot{}),
-               "P1");
-        },
+        [&] { ck(fdg::launch_hartley_row(st, lc, a->r.d(), a->u.d(), F, pc->n2, pc->tab.tw_2, nullptr, RedSlot{}),
+                 "P1"); },
         [&] { ck(fdg::launch_hartley_col(st, lc, a->u.d(), pc->nt, pc->n1, pc->n2, pc->tab.tw_1), "P2"); },
         [&] { ck(fdg::launch_t_filter(st, lc, a->u.d(), pc->tab), "P3"); },
         [&] { ck(fdg::launch_hartley_col(st, lc, a->u.d(), pc->nt, pc->n1, pc->n2, pc->tab.tw_1), "P4"); },
-        [&] {
-          if (pipe)
-            ck(fdg::launch_pc_pipe(st, lc, a->u.d(), a->u.d(), a->z.d(), a->r.d(), sc.slot(S_DOT), pc->nt, pc->n1,
-                                   pc->tab.tw_1, ready, false),
-               "P45");
-          else
-            ck(fdg::launch_hartley_row(st, lc, a->u.d(), a->z.d(), F, pc->n2, pc->tab.tw_2, a->r.d(), sc.slot(S_DOT)),
-               "P5");
-        },
+        [&] { ck(fdg::launch_hartley_row(st, lc, a->u.d(), a->z.d(), F, pc->n2, pc->tab.tw_2, a->r.d(), sc.slot(S_DOT)),
+                 "P5"); },
         [&] { ck(fdg::launch_axpy_dev(st, lc, a->tmp.d(), a->d.d(), N, sc.at(S_RZ0), sc.at(S_PQ)), "X"); },
     };
     // algorithmic HBM bytes per launch (each N-vector read or written once)
@@ -1814,11 +1782,6 @@ fdg_status fdg_admm_profile_passes(fdg_admm a, int reps, double* ms, double* byt
     const double k1 = op->tf.kind != 2 ? 6 * nb : 2 * nb;
     double alg[9] = {k1, 4 * nb, 4 * nb, 2 * nb, 2 * nb, 2 * nb, 2 * nb, 3 * nb, 3 * nb};
     for (size_t i = 0; i < passes.size(); ++i) {
-      if (pipe && (i == 4 || i == 6)) {  // P2 / P4 run inside the fused P1 / P5 kernels
-        ms[i] = 0.0;
-        if (bytes) bytes[i] = 0.0;
-        continue;
-      }
       passes[i]();  // warm
       ck(cudaEventRecord(a->e0, st), "event");
       for (int r = 0; r < reps; ++r) passes[i]();

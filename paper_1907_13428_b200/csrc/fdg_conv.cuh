@@ -29,20 +29,6 @@
 
 namespace fdg {
 
-// timing experiment: FDG_EXP_NOIO drops the global traffic (numerically invalid)
-#ifdef FDG_EXP_NOIO
-#define FDG_IO(x) \
-  do {                        \
-    if (a.scale == 12345.0) { \
-      x;                      \
-    }                         \
-  } while (0)
-#else
-#define FDG_IO(x) \
-  do {            \
-    x;            \
-  } while (0)
-#endif
 
 #ifndef FDG_C512_THREADS
 #define FDG_C512_THREADS 128
@@ -223,30 +209,21 @@ __device__ __forceinline__ void conv_half(double2 (&v)[CCfg<L>::R], Ex& ex, int 
   using C = CCfg<L>;
   constexpr int M = C::M, R = C::R, T = C::T, G2 = C::G2;
   constexpr bool CACHE = FDG_TWCACHE && TwCache<M, R>::OK;
-#ifdef FDG_EXP_NOCONV
-  return;
-#endif
-#ifndef FDG_EXP_NOTWIST
   if (b) {
 #pragma unroll
     for (int m = 0; m < R; ++m) v[m] = cmul(v[m], twist[t + T * m]);
   }
-#endif
   double2 wc[TwCache<M, R>::K];
   fft_lane_c<M, R, G2, false, LAYOUT, CACHE ? 1 : 0>(v, ex, t, gs, tw, wc);
-#ifndef FDG_EXP_NOSYM
 #pragma unroll
   for (int m = 0; m < R; ++m) v[m] = sym.apply(v[m], 2 * (t + T * m) + b);
-#endif
   fft_lane_c<M, R, G2, true, LAYOUT, CACHE ? 2 : 0>(v, ex, t, gs, tw, wc);
-#ifndef FDG_EXP_NOTWIST
   // FDG_BAL_TWIST: the odd half's post-twist W_L^-j is applied in
   // conv_combine, each half twisting the odd values of its own positions
   if (b && !FDG_BAL_TWIST) {
 #pragma unroll
     for (int m = 0; m < R; ++m) v[m] = cmulc(v[m], twist[t + T * m]);
   }
-#endif
 }
 
 // Adds the two halves: half 0 owns positions t + T m for m < R/2, half 1
@@ -263,11 +240,6 @@ __device__ __forceinline__ void conv_combine(const double2 (&v)[CCfg<L>::R], dou
   using C = CCfg<L>;
   constexpr int M = C::M, T = C::T, G2 = C::G2, HR = C::HR;
   const int t = mp.t, b = mp.b;
-#ifdef FDG_EXP_NOCOMB
-#pragma unroll
-  for (int i = 0; i < HR; ++i) y[i] = b ? v[i + HR] : v[i];
-  return;
-#endif
   pair_sync<L, LAYOUT, HM>(mp.g);  // write-after-read: last inverse-FFT exchange
   double2* sm = ex.next();
 #pragma unroll
@@ -281,7 +253,7 @@ __device__ __forceinline__ void conv_combine(const double2 (&v)[CCfg<L>::R], dou
     const int pos = t + T * (i + b * HR);
     double2 mine = b ? v[i + HR] : v[i];
     double2 other = sm[slot<LAYOUT, M, G2>(pos, mp.partner)];
-#if FDG_BAL_TWIST && !defined(FDG_EXP_NOTWIST)
+#if FDG_BAL_TWIST
     const double2 w = twist[pos];
     if (b) mine = cmulc(mine, w);
     else other = cmulc(other, w);
@@ -358,8 +330,8 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
   };
   if constexpr (PF) {
     if (blockIdx.x < ntiles) {
-      FDG_IO(stage_rows(st_in, in0 + (size_t)blockIdx.x * 2 * G * n, TILE));
-      if (MODE == 2 && !first) FDG_IO(stage_rows(st_in2, in1 + (size_t)blockIdx.x * 2 * G * n, TILE));
+      stage_rows(st_in, in0 + (size_t)blockIdx.x * 2 * G * n, TILE);
+      if (MODE == 2 && !first) stage_rows(st_in2, in1 + (size_t)blockIdx.x * 2 * G * n, TILE);
       if (upd_x) load_x(blockIdx.x);
     }
     cp_async_commit();
@@ -387,13 +359,13 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
             z.y += beta * dd.y;
           }
           if ((m < HR) == (b == 0)) {
-            FDG_IO(a.dnew[ra + pos] = z.x);
-            FDG_IO(a.dnew[ra + n + pos] = z.y);
+            a.dnew[ra + pos] = z.x;
+            a.dnew[ra + n + pos] = z.y;
             if constexpr (XPF) {
               if (upd_x) {
                 const int i = m < HR ? m : m - HR;  // static: only the owning half stores
-                FDG_IO(a.xs[ra + pos] = xpre[i].x + alpha * dd.x);
-                FDG_IO(a.xs[ra + n + pos] = xpre[i].y + alpha * dd.y);
+                a.xs[ra + pos] = xpre[i].x + alpha * dd.x;
+                a.xs[ra + n + pos] = xpre[i].y + alpha * dd.y;
               }
             }
           }
@@ -408,19 +380,19 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
       tile_nb = a.tkind == 1 && (a.tdir < 0 ? k >= 1 : k + 1 < a.nt);
       if constexpr (SEPI) {
         if (tile_nb) {
-          FDG_IO(stage_rows(st_nb, in0 + (size_t)f0 * n + noff, TILE));
-          if (MODE == 2 && !first) FDG_IO(stage_rows(st_nb2, in1 + (size_t)f0 * n + noff, TILE));
+          stage_rows(st_nb, in0 + (size_t)f0 * n + noff, TILE);
+          if (MODE == 2 && !first) stage_rows(st_nb2, in1 + (size_t)f0 * n + noff, TILE);
         }
         if constexpr (MODE == 1) {
-          FDG_IO(stage_rows(st_vp, a.vp + (size_t)f0 * n, TILE));
-          if (a.r) FDG_IO(stage_rows(st_r, (a.r_in ? a.r_in : a.r) + (size_t)f0 * n, TILE));
+          stage_rows(st_vp, a.vp + (size_t)f0 * n, TILE);
+          if (a.r) stage_rows(st_r, (a.r_in ? a.r_in : a.r) + (size_t)f0 * n, TILE);
         }
       }
       cp_async_commit();  // group E
       const int nxt = tile + gridDim.x;
       if (nxt < ntiles) {
-        FDG_IO(stage_rows(st_in, in0 + (size_t)nxt * 2 * G * n, TILE));
-        if (MODE == 2 && !first) FDG_IO(stage_rows(st_in2, in1 + (size_t)nxt * 2 * G * n, TILE));
+        stage_rows(st_in, in0 + (size_t)nxt * 2 * G * n, TILE);
+        if (MODE == 2 && !first) stage_rows(st_in2, in1 + (size_t)nxt * 2 * G * n, TILE);
       }
       cp_async_commit();  // group I
     } else {
@@ -437,8 +409,8 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
               if (vb) z.y += beta * __ldg(in1 + ra + n + pos);
             }
             if ((m < HR) == (b == 0)) {
-              if (va) FDG_IO(a.dnew[ra + pos] = z.x);
-              if (vb) FDG_IO(a.dnew[ra + n + pos] = z.y);
+              if (va) a.dnew[ra + pos] = z.x;
+              if (vb) a.dnew[ra + n + pos] = z.y;
             }
           }
         }
@@ -480,14 +452,14 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
           }
         }
         if constexpr (MODE == 0 || MODE == 2) {
-          FDG_IO(a.out[o] = val);
-          if (MODE == 2 && !XPF && a.upd_x && !first) FDG_IO(a.xs[o] += alpha * __ldg(in1 + o));
+          a.out[o] = val;
+          if (MODE == 2 && !XPF && a.upd_x && !first) a.xs[o] += alpha * __ldg(in1 + o);
         } else {
           const double q = (SEPI ? st_vp[sl] : __ldg(&a.vp[o])) + val;
           if (a.q_out) a.q_out[o] = q;
           if (a.r) {
             const double rn = (SEPI ? st_r[sl] : (a.r_in ? a.r_in : a.r)[o]) - alpha * q;
-            FDG_IO(a.r[o] = rn);
+            a.r[o] = rn;
             acc += rn * rn;
           }
         }
@@ -548,8 +520,8 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
   };
   if constexpr (PF) {
     if (blockIdx.x < ntiles) {
-      FDG_IO(stage_tile(S.stage, a.x, blockIdx.x));
-      if constexpr (MODE == 2) FDG_IO(stage_tile(S.stage + 2 * TILE, a.acc, blockIdx.x));
+      stage_tile(S.stage, a.x, blockIdx.x);
+      if constexpr (MODE == 2) stage_tile(S.stage + 2 * TILE, a.acc, blockIdx.x);
     }
     cp_async_commit();
   }
@@ -573,8 +545,8 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
       for (int m = 0; m < R; ++m) v[m] = *reinterpret_cast<const double2*>(st_in + (t + m * T) * P + 2 * g);
       if constexpr (MODE != 2) __syncthreads();  // single input buffer
       if (nxt < ntiles) {
-        FDG_IO(stage_tile(S.stage + (buf ^ DB) * TILE, a.x, nxt));
-        if constexpr (MODE == 2) FDG_IO(stage_tile(S.stage + (2 + (buf ^ 1)) * TILE, a.acc, nxt));
+        stage_tile(S.stage + (buf ^ DB) * TILE, a.x, nxt);
+        if constexpr (MODE == 2) stage_tile(S.stage + (2 + (buf ^ 1)) * TILE, a.acc, nxt);
       }
       cp_async_commit();
     } else {
@@ -596,7 +568,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
         const size_t o2 = base + (size_t)pos * C;
         double2 acc = make_double2(0.0, 0.0);
         if (a.acc) acc = col_get<PF>(a.acc + o2, C, c);
-        FDG_IO(col_put<PF>(a.out + o2, C, c, make_double2(acc.x + a.scale * y[i].x, acc.y + a.scale * y[i].y)));
+        col_put<PF>(a.out + o2, C, c, make_double2(acc.x + a.scale * y[i].x, acc.y + a.scale * y[i].y));
       }
     } else {
       // S mid pass: Bp = u + scale L1 p; w = Bp / m2[o] (-> a.w, and the
@@ -614,7 +586,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
           const double wx = bx * im2, wy = vb ? by * im2 : 0.0;
           e += a1 * pv.x * pv.x + wx * bx;
           if (vb) e += a1 * pv.y * pv.y + wy * by;
-          FDG_IO(col_put<PF>(a.w + o2, C, c, make_double2(wx, wy)));
+          col_put<PF>(a.w + o2, C, c, make_double2(wx, wy));
           y[i] = make_double2(wx, wy);
         } else {
           y[i] = make_double2(0.0, 0.0);
@@ -643,7 +615,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
         if (!PF && (pos >= n || !vc)) continue;
         const size_t o2 = base + (size_t)pos * C;
         const double2 pv = PF ? *reinterpret_cast<const double2*>(st_in + pos * P + 2 * g) : col_get<PF>(a.x + o2, C, c);
-        FDG_IO(col_put<PF>(a.out + o2, C, c, make_double2(a.scale * y[i].x + a1 * pv.x, a.scale * y[i].y + a1 * pv.y)));
+        col_put<PF>(a.out + o2, C, c, make_double2(a.scale * y[i].x + a1 * pv.x, a.scale * y[i].y + a1 * pv.y));
       }
     }
   }

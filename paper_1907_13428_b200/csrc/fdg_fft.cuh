@@ -369,22 +369,15 @@ struct Stockham {
             for (int r = 1; r < Rp; ++r) wc[s * Rp + r] = wt[r];
           }
         }
-#ifndef FDG_EXP_NOMATH
 #pragma unroll
         for (int r = 1; r < Rp; ++r) v[s + r * S] = INV ? cmulc(v[s + r * S], wt[r]) : cmul(v[s + r * S], wt[r]);
-#else
-        v[s + S] = cadd(v[s + S], wt[1]);
-#endif
       }
-#ifndef FDG_EXP_NOMATH
       Dft<Rp, INV>::run(v, s, S);
-#endif
     }
     if constexpr (!LAST) {
       if (ex.single()) lane_sync<LAYOUT, T, G>(g);  // write-after-read on the single buffer
       double2* sm = ex.next();
       // scatter: out[(b/Ns)*Ns*Rp + b%Ns + r*Ns] = v[s + r*S]
-#ifndef FDG_EXP_NOEX
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const int b = t + s * T;
@@ -392,12 +385,9 @@ struct Stockham {
 #pragma unroll
         for (int r = 0; r < Rp; ++r) sm[slot<LAYOUT, N, G>(base + r * Ns, g)] = v[s + r * S];
       }
-#endif
       lane_sync<LAYOUT, T, G>(g);
-#ifndef FDG_EXP_NOEX
 #pragma unroll
       for (int m = 0; m < R; ++m) v[m] = sm[slot<LAYOUT, N, G>(t + m * T, g)];
-#endif
       Stockham<N, R, G, INV, Ns * Rp, LAYOUT, NEXT_OFF, CM>::run(v, ex, t, g, ptw, wc);
     }
   }

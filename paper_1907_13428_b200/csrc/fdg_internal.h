@@ -104,14 +104,6 @@ cudaError_t launch_hartley_col(cudaStream_t st, LaunchCounter* lc, double* data,
 cudaError_t launch_t_filter(cudaStream_t st, LaunchCounter* lc, double* data, const PcTables& pt,
                             const int* guard = nullptr);
 
-// Fused preconditioner axis pairs through L2 (fdg_pcfused.cuh), n1 == n2 == n
-// in {256, 512}: rows_first = 1: x2 then x1 (in -> mid == out); 0: x1 in place
-// on mid (== in) then x2 -> out with r.z into red.  ready: nt + 1 ints, zero.
-bool pc_pipe_supported(int n1, int n2);
-cudaError_t launch_pc_pipe(cudaStream_t st, LaunchCounter* lc, const double* in, double* mid, double* out,
-                           const double* rdot, RedSlot red, int nt, int n, const double2* tw, int* ready,
-                           bool rows_first, const int* guard = nullptr);
-
 // PCG control of one speculative iteration (1 thread): out[0] = pq,
 // out[1] = |r|^2 (copied for the host); raises *pause when the host must act
 // (pq <= 0 / non-finite, non-finite residual, or |r| <= tol |b|).

@@ -175,9 +175,6 @@ cudaError_t run_row_v(cudaStream_t st, const RowArgs& a) {
 #ifndef FDG_QSPLIT
 #define FDG_QSPLIT 1
 #endif
-#ifndef FDG_SPLIT_RAGGED
-#define FDG_SPLIT_RAGGED 0
-#endif
 // Q-split passes (fdg_convq.cuh) for full tiles with real symbols.  Rows at
 // L = 1024 only: measured at 128 x 512^2 K3 383 -> 369 us, K1 equal; at
 // L = 2048 (Q = 8) the input/output combinations and the scattered twist
@@ -224,12 +221,6 @@ cudaError_t run_row(cudaStream_t st, const RowArgs& a) {
         if constexpr (RowCPlan<L, MODE, true, false>::SMEM <= kMaxSmem) return run_rowc_s<L, MODE, true, false>(st, a);
       }
     }
-#if FDG_SPLIT_RAGGED
-    if (2 * a.n > L / 2 + 1) {  // ragged n (e.g. C1's 1023): unstaged split pass
-      if (a.sym_re) return run_rowc_s<L, MODE, false, true>(st, a);
-      return run_rowc_s<L, MODE, false, false>(st, a);
-    }
-#endif
     return run_row_direct<L, MODE, false>(st, a);
   } else {
     if constexpr (Cfg<L>::PF_OK) {
@@ -254,9 +245,6 @@ cudaError_t run_col_v(cudaStream_t st, const ColArgs& a) {
   return run_col_direct<L, MODE, PF>(st, a);
 }
 
-#ifndef FDG_PF_COL2048
-#define FDG_PF_COL2048 0  // 1: spills at 128 registers (measured 4.1 vs 3.2 ms at C4)
-#endif
 #ifndef FDG_SPLIT_COL_LMAX
 #define FDG_SPLIT_COL_LMAX 2048  // L = 2048 split column tiles (W = 4): K2 3195 -> 3169 us at C4 in the chain
 #endif
@@ -270,17 +258,10 @@ cudaError_t run_col(cudaStream_t st, const ColArgs& a) {
         if constexpr (ColCPlan<L, MODE, true, false>::SMEM <= kMaxSmem) return run_colc_s<L, MODE, true, false>(st, a);
       }
     }
-#if FDG_SPLIT_RAGGED
-    if (2 * a.n > L / 2 + 1) {
-      if (a.sym_re) return run_colc_s<L, MODE, false, true>(st, a);
-      return run_colc_s<L, MODE, false, false>(st, a);
-    }
-#endif
     return run_col_direct<L, MODE, false>(st, a);
   } else {
-    // staged full tiles for the direct column kernel also at L = 2048 (the
-    // unstaged x1 pass of C4 stalls on global loads: long_scoreboard 5.6)
-    if constexpr (Cfg<L>::PF_OK || (L == 2048 && FDG_PF_COL2048)) {
+    // staged full tiles for the direct column kernel where they fit
+    if constexpr (Cfg<L>::PF_OK) {
       if (2 * a.n == L && a.C % (2 * Cfg<L>::G) == 0) return run_col_v<L, MODE, true>(st, a);
     }
     return run_col_v<L, MODE, false>(st, a);
