@@ -1,7 +1,8 @@
 """Summaries of the ncu captures for profiles/ (run here on the merged
 gpurun_out/ files).
 
-  python scripts/ncu_summary.py full REPORT.ncu-rep OUT.csv TRAFFIC.json
+  python scripts/ncu_summary.py full REPORT.ncu-rep OUT.csv TRAFFIC.json "nt n1 n2" [LABEL]
+      (merges the per-pass DRAM traffic into TRAFFIC.json under the key "ntxn1xn2")
   python scripts/ncu_summary.py launches LAUNCHES.csv OUT.csv "command"
 """
 import csv
@@ -11,9 +12,8 @@ import subprocess
 import sys
 from collections import OrderedDict
 
-N_C2 = 256 ** 3
 # algorithmic N-vector passes per launch (SURVEY.md 8d / DESIGN.md)
-ALG = {"K1_row_p_update_B": 4, "K2_col_S_mid": 4, "K3_row_BT_update": 4, "P1_hartley_x2": 2,
+ALG = {"K1_row_p_update_B": 6, "K2_col_S_mid": 4, "K3_row_BT_update": 4, "P1_hartley_x2": 2,
        "P2_hartley_x1": 2, "P3_t_filter": 2, "P4_hartley_x1": 2, "P5_hartley_x2_dot": 3, "X_axpy": 3}
 
 
@@ -43,7 +43,10 @@ def f(x):
         return float("nan")
 
 
-def full(rep, out_csv, traffic_json):
+def full(rep, out_csv, traffic_json, shape="256 256 256", label="C2"):
+    dims = [int(v) for v in shape.split()]
+    n_elem = dims[0] * dims[1] * dims[2]
+    key = "x".join(str(v) for v in dims)
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
@@ -55,12 +58,12 @@ def full(rep, out_csv, traffic_json):
         if m not in ix:
             return float("nan")
         return f(r[ix[m]]) * scale.get(units[ix[m]], 1.0)
-    seen, out, traffic = {}, [], OrderedDict()
+    seen, out, traffic, fp64, issue = {}, [], OrderedDict(), OrderedDict(), OrderedDict()
     for r in data:
         name = pass_name(r[ix["Kernel Name"]], seen)
         us = g(r, "gpu__time_duration.sum")
         rd, wr = g(r, "dram__bytes_read.sum"), g(r, "dram__bytes_write.sum")
-        alg = ALG.get(name, float("nan")) * 8 * N_C2
+        alg = ALG.get(name, float("nan")) * 8 * n_elem
         out.append([name, r[ix["Kernel Name"]].split("(")[0].replace("void ", ""), f"{us:.1f}",
                     f"{rd / 1e6:.1f}", f"{wr / 1e6:.1f}", f"{(rd + wr) / 1e6:.1f}", f"{alg / 1e6:.1f}",
                     f"{(rd + wr) / alg:.2f}", f"{(rd + wr) / (us * 1e-6) / 1e9:.0f}",
@@ -72,17 +75,24 @@ def full(rep, out_csv, traffic_json):
                     f"{g(r, 'launch__registers_per_thread'):.0f}"])
         if name in ALG and name not in traffic:
             traffic[name] = rd + wr
+            fp64[name] = round(g(r, 'sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active'), 1)
+            issue[name] = round(g(r, 'smsp__issue_active.avg.pct_of_peak_sustained_active'), 1)
     with open(out_csv, "w") as fh:
-        fh.write(f"# ncu --set full summary (C2 256^3, kernels of one PCG iteration; {rep.split('/')[-1]})\n")
+        fh.write(f"# ncu --set full summary ({label} {key}, kernels of one PCG iteration; {rep.split('/')[-1]})\n")
         fh.write("# traffic = dram__bytes_read.sum + dram__bytes_write.sum per launch; alg = algorithmic bytes\n")
         w = csv.writer(fh)
         w.writerow(["pass", "kernel", "us", "dram_read_MB", "dram_write_MB", "traffic_MB", "alg_MB",
                     "traffic/alg", "dram_GBs", "fp64_pipe_pct", "warps_active_pct", "issue_active_pct",
                     "l1tex_throughput_pct", "smem_wavefronts_M", "regs"])
         w.writerows(out)
-    traffic["_source"] = f"{out_csv} (ncu --set full, C2 256^3)"
+    try:
+        allcap = json.load(open(traffic_json))
+    except Exception:  # noqa: BLE001
+        allcap = {}
+    allcap[key] = {"source": f"{out_csv} (ncu --set full, {label} {key})", "traffic": traffic,
+                   "fp64_pipe_pct": fp64, "issue_active_pct": issue}
     with open(traffic_json, "w") as fh:
-        json.dump(traffic, fh, indent=1)
+        json.dump(allcap, fh, indent=1)
     for row in out:
         print(",".join(row))
 
@@ -118,6 +128,6 @@ def launches(log, out_csv, cmd):
 
 if __name__ == "__main__":
     if sys.argv[1] == "full":
-        full(*sys.argv[2:5])
+        full(*sys.argv[2:7])
     else:
         launches(*sys.argv[2:5])

@@ -1,11 +1,14 @@
-"""One C2 PCG solve (for ncu captures of the hot kernels)."""
+"""One PCG solve of a BASELINE config (for ncu captures of the hot kernels).
+CONFIG=C2|C3|C4 (real parameters; default C2), SHAPE="nt n1 n2" overrides the
+grid, MAXIT caps the Krylov iterations (default 3)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_1907_13428_b200 import Context, make_problem
-shape = tuple(int(v) for v in os.environ.get("SHAPE", "256 256 256").split())
+name = os.environ.get("CONFIG", "C2")
+shape = tuple(int(v) for v in os.environ["SHAPE"].split()) if "SHAPE" in os.environ else None
 ctx = Context(0)
-c, op, pc, drv = make_problem("C2", shape, ctx=ctx)
+c, op, pc, drv = make_problem(name, shape, ctx=ctx)
 N = op.size
 rhs = torch.empty(N, dtype=torch.float64, device="cuda")
 x = torch.zeros_like(rhs)
