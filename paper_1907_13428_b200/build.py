@@ -15,7 +15,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib", "libfdg.so")
-SOURCES = ["fdg_kernels.cu", "fdg_api.cu"] + sorted(
+SOURCES = ["fdg_kernels.cu", "fdg_api.cu", "fdg_pfa.cu"] + sorted(
     f for f in os.listdir(CSRC) if f.startswith("fdg_inst_") and f.endswith(".cu"))
 HEADERS = [f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

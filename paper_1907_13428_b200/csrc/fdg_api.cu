@@ -471,6 +471,16 @@ void pc2_apply_dev(fdg_pc_s* pc, const double* r, double* z) {
   double* u = pc->bu.d();
   double* v = pc->bv.d();
   TimeFactor none;
+#ifndef FDG_PFA
+#define FDG_PFA 1
+#endif
+  if (FDG_PFA && fdg::pfa_supported(n1) && fdg::pfa_supported(n2)) {
+    // 1023 = 33 x 31: three prime-factor Hartley passes (fdg_pfa.cu)
+    ck(fdg::launch_pfa_hrow(st, lc, r, u, F, 1.0), "pc2 pfa x2");
+    ck(fdg::launch_pfa_hcol(st, lc, u, pc->nt, n2, pc->lam1.d(), pc->lam2.d()), "pc2 pfa x1");
+    ck(fdg::launch_pfa_hrow(st, lc, u, z, F, 1.0 / ((double)n1 * n2)), "pc2 pfa x2 out");
+    return;
+  }
   if (F == Fp) {  // the pre-chirp rides in the convolution's load (k_row<.., CH>)
     ck(fdg::launch_row_apply(st, lc, r, v, 1, Fp, n2, pc->bs2, 1.0 / pc->bs2.L, none, 1.0, false, c2),
        "pc2 x2 pre + conv");

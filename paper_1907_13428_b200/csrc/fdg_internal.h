@@ -186,6 +186,13 @@ cudaError_t launch_objective(cudaStream_t st, LaunchCounter* lc, const double* y
 // Bluestein stages of the 2-level spatial preconditioner (fdg_kernels.cu).
 // F = nt * n1 real rows; row-pair buffers are [F rounded up to even][n2],
 // column-pair buffers [nt][n1][P2] with P2 = n2 rounded up to even.
+// 1023-point prime-factor Hartley passes of the 2-level preconditioner
+// (fdg_pfa.cu): rows out = scale * H2 in; columns in place H1 / lambda / H1.
+bool pfa_supported(int n);
+cudaError_t launch_pfa_hrow(cudaStream_t st, LaunchCounter* lc, const double* in, double* out, long F,
+                            double scale);
+cudaError_t launch_pfa_hcol(cudaStream_t st, LaunchCounter* lc, double* data, int nt, int C, const double* lam1,
+                            const double* lam2);
 cudaError_t launch_bs_pre_rows(cudaStream_t st, LaunchCounter* lc, const double* in, double* out, long F, int n2,
                                const double2* c2);
 cudaError_t launch_bs_rows_to_cols(cudaStream_t st, LaunchCounter* lc, const double* v, double* u, long F, int n1,

@@ -1,0 +1,371 @@
+// fdg_pfa.cu — 1023-point prime-factor Hartley passes of the 2-level T. Chan
+// preconditioner (BASELINE config 1: 256 slices of 1023 x 1023).
+//
+// Reference: the per-level circulant solve of CirculantPreconditioner
+// (circulant.cpp:49-67: forward DFT, divide by the eigenvalues, inverse DFT)
+// restricted to the two spatial levels, with the level eigenvalues of
+// circulant.cpp:10-26.  The eigenvalues of the T. Chan circulants of the
+// symmetric Riesz factors are real and even, so per slice
+//   z = (1 / (n1 n2)) H2 H1 D H1 H2 r,   D[k][j] = 1 / (lam1[k] + lam2[j])
+// with H the real Hartley transform along an axis; this is
+// what the generic Bluestein path (fdg_api.cu pc2_apply_dev) evaluates in 9
+// passes for any level size.  For n = 1023 = 33 x 31 (33 = 3 x 11) the DFT
+// has a twiddle-free prime-factor (Good-Thomas) decomposition, so each
+// Hartley transform is a register-resident DFT_31 pass, one shared-memory
+// exchange and a register-resident DFT_33 (= DFT_3 x DFT_11) pass:
+//   input  n = (31 a + 33 b) mod 1023          a < 33, b < 31
+//   output k = (496 k1 + 528 k2) mod 1023       (496 = 31 (31^-1 mod 33), 528 = 33 (33^-1 mod 31))
+//   X[k] = sum_a W33^(a k1) sum_b W31^(b k2) x[n]
+// and inside DFT_33: a = (11 i + 3 j) mod 33, k1 = (22 c + 12 d) mod 33.
+// Three passes, 6N doubles of HBM traffic (SURVEY 8d's 2-level model):
+//   k_pfa_hrow  (rows, x2):  r -> H2 r
+//   k_pfa_hcol  (columns, x1, in place): H1 -> divide by lam1[k] + lam2[j] -> H1
+//   k_pfa_hrow  (rows, x2):  -> (1 / (n1 n2)) H2, = z
+// Lane = two real fibres packed as a + i b (one complex DFT, Hartley split by
+// the mirror X[N - k]).  A lane is served by 33 threads: thread a runs the
+// DFT_31 of input column a, thread k2 < 31 the DFT_33 of output row k2.  A
+// CTA holds G = 7 lanes (231 working threads of 256): staging for the next
+// tile (2G fibres, cp.async) + one exchange area (G lanes), 224 KB.
+#include <cuda_runtime.h>
+
+#include "fdg_fft.cuh"
+#include "fdg_internal.h"
+#include "fdg_launch.cuh"
+#include "fdg_passes.cuh"
+#include "fdg_pfa_tab.h"
+
+namespace fdg {
+namespace {
+
+constexpr int PN = 1023;     // transform length
+constexpr int PA = 33;       // outer factor (3 x 11), threads per lane
+constexpr int PB = 31;       // inner factor
+constexpr int PG = 7;        // lanes per CTA
+constexpr int PTHREADS = 256;
+constexpr size_t PSMEM = 2 * (size_t)PG * PN * sizeof(double2);
+
+// cos / sin (2 pi j / P), j < P (fdg_pfa_tab.h, scripts/gen_pfa_consts.py)
+__constant__ double kC3[3] = FDG_PFA_C3;
+__constant__ double kS3[3] = FDG_PFA_S3;
+__constant__ double kC11[11] = FDG_PFA_C11;
+__constant__ double kS11[11] = FDG_PFA_S11;
+__constant__ double kC31[31] = FDG_PFA_C31;
+__constant__ double kS31[31] = FDG_PFA_S31;
+
+template <int P>
+__device__ __forceinline__ double twc(int j) {
+  return P == 3 ? kC3[j] : (P == 11 ? kC11[j] : kC31[j]);
+}
+template <int P>
+__device__ __forceinline__ double tws(int j) {
+  return P == 3 ? kS3[j] : (P == 11 ? kS11[j] : kS31[j]);
+}
+
+// cos / sin (2 pi k m / 31) for m, k = 1..15: the DFT_31 output loop runs
+// over m at run time (uniform constant loads), which keeps ptxas from
+// interleaving all 15 outputs and spilling.
+struct Tab31 {
+  double c[15][15], s[15][15];
+};
+__constant__ Tab31 kT31 = {FDG_PFA_T31C, FDG_PFA_T31S};
+
+// Forward DFT of odd prime length P in place (natural order), X_m =
+// sum_n x_n exp(-2 pi i n m / P), by the symmetric pair algorithm:
+// s_k = x_k + x_{P-k}, d_k = x_k - x_{P-k};  X_m = A_m - i B_m,
+// X_{P-m} = A_m + i B_m with A_m = x_0 + sum_k cos(2 pi k m / P) s_k and
+// B_m = sum_k sin(2 pi k m / P) d_k.
+template <int P, class Put>
+__device__ __forceinline__ void dft_odd(const double2 (&x)[P], Put&& put) {
+  constexpr int H = (P - 1) / 2;
+  double2 s[H], d[H];
+#pragma unroll
+  for (int k = 1; k <= H; ++k) {
+    s[k - 1] = cadd(x[k], x[P - k]);
+    d[k - 1] = csub(x[k], x[P - k]);
+  }
+  const double2 x0 = x[0];
+  double2 sum = x0;
+#pragma unroll
+  for (int k = 0; k < H; ++k) sum = cadd(sum, s[k]);
+  put(0, sum);
+  if constexpr (P == 31) {
+#pragma unroll 1
+    for (int m = 1; m <= H; ++m) {
+      const double c0 = kT31.c[m - 1][0], s0 = kT31.s[m - 1][0];
+      double2 A = make_double2(fma(c0, s[0].x, x0.x), fma(c0, s[0].y, x0.y));
+      double2 B = make_double2(s0 * d[0].x, s0 * d[0].y);
+#pragma unroll
+      for (int k = 2; k <= H; ++k) {
+        const double c = kT31.c[m - 1][k - 1], sn = kT31.s[m - 1][k - 1];
+        A.x = fma(c, s[k - 1].x, A.x);
+        A.y = fma(c, s[k - 1].y, A.y);
+        B.x = fma(sn, d[k - 1].x, B.x);
+        B.y = fma(sn, d[k - 1].y, B.y);
+      }
+      put(m, make_double2(A.x + B.y, A.y - B.x));
+      put(P - m, make_double2(A.x - B.y, A.y + B.x));
+    }
+    return;
+  }
+#pragma unroll
+  for (int m = 1; m <= H; ++m) {
+    double2 A = x0, B;
+#pragma unroll
+    for (int k = 1; k <= H; ++k) {
+      const int j = (k * m) % P;
+      const double c = twc<P>(j), sn = tws<P>(j);
+      A.x = fma(c, s[k - 1].x, A.x);
+      A.y = fma(c, s[k - 1].y, A.y);
+      if (k == 1) {
+        B = make_double2(sn * d[0].x, sn * d[0].y);
+      } else {
+        B.x = fma(sn, d[k - 1].x, B.x);
+        B.y = fma(sn, d[k - 1].y, B.y);
+      }
+    }
+    // outputs leave as soon as they are formed (the inputs stay live)
+    put(m, make_double2(A.x + B.y, A.y - B.x));
+    put(P - m, make_double2(A.x - B.y, A.y + B.x));
+  }
+}
+
+// Opaque copy of a loop-invariant value: index arithmetic derived from it is
+// recomputed per tile instead of being hoisted out of the tile loop (31 + 62
+// hoisted gather / mirror offsets push the kernels into spills).
+__device__ __forceinline__ int opaque(int v) {
+  int r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+
+// Slot of X[k] in the exchange area after pfa_dft (CRT order).
+__device__ __forceinline__ int xslot(int k) { return (k % PB) * PA + k % PA; }
+
+// Pass-A gather of one real fibre: v[b] = x[(31 a + 33 b) mod 1023], a = t.
+template <class F>
+__device__ __forceinline__ void pfa_gather(double (&v)[PB], int t, F&& src) {
+  int idx = 31 * t;
+#pragma unroll
+  for (int b = 0; b < PB; ++b) {
+    v[b] = src(idx);
+    idx += 33;
+    if (idx >= PN) idx -= PN;
+  }
+}
+
+// The lane's DFT of x = xa + i xb (two real fibres read by srca / srcb(n))
+// into the lane's exchange area E (1023 double2), X[k] at E[xslot(k)].
+// Every thread of the CTA calls it (CTA barriers inside); `act`: the thread
+// serves a lane (thread a = t < 33 of pass A, k2 = t < 31 of pass B).
+// `freed()` runs once every gather is done (the source area may be reused;
+// E is written only after it).
+template <class FA, class FB, class FR>
+__device__ __forceinline__ void pfa_dft(double2* E, int t, bool act, FA&& srca, FB&& srcb, FR&& freed) {
+  // Idle threads (no lane, or t >= 31 in pass B) run the same code on valid
+  // addresses with their stores predicated off: branch-free blocks keep
+  // ptxas' register allocation spill-free.
+  double va[PB], vb[PB];
+  pfa_gather(va, t, srca);
+  pfa_gather(vb, t, srcb);
+  __syncthreads();
+  freed();
+  {
+    double2 v[PB];
+#pragma unroll
+    for (int b = 0; b < PB; ++b) v[b] = make_double2(va[b], vb[b]);
+    // E[k2 * 33 + a]: pass-B thread k2 reads 33 consecutive entries
+    dft_odd<PB>(v, [&](int k2, double2 val) {
+      if (act) E[k2 * PA + t] = val;
+    });
+  }
+  __syncthreads();
+  const bool actb = act && t < PB;
+  const int tb = t < PB ? t : PB - 1;
+  double2 r[3][11];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 11; ++j) r[i][j] = E[tb * PA + (11 * i + 3 * j) % PA];
+  __syncthreads();  // every pass-B read done: E is overwritten with X below
+#pragma unroll
+  for (int j = 0; j < 11; ++j) {
+    const double2 u[3] = {r[0][j], r[1][j], r[2][j]};
+    dft_odd<3>(u, [&](int c, double2 val) { r[c][j] = val; });
+  }
+  // X[k] with k = k1 (mod 33), k = k2 (mod 31) at E[k2 * 33 + k1]
+  // (k1 = (22 c + 12 d) mod 33, k2 = t)
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    dft_odd<11>(r[c], [&](int d, double2 val) {
+      if (actb) E[tb * PA + (22 * c + 12 * d) % PA] = val;
+    });
+  __syncthreads();
+}
+
+// Row pass along x2 (rows of 1023 contiguous doubles): out = scale * H2 in.
+__global__ void __launch_bounds__(PTHREADS, 1)
+    k_pfa_hrow(const double* __restrict__ in, double* __restrict__ out, long F, double scale) {
+  extern __shared__ double2 smem_raw[];
+  double* S = reinterpret_cast<double*>(smem_raw);  // 2G fibres of the tile
+  double2* Ex = smem_raw + PG * PN;                  // G lanes
+  pdl_trigger();
+  pdl_wait();
+  const int tid = threadIdx.x;
+  const int g = tid / PA, t0 = tid - g * PA;
+  const bool act = g < PG;
+  const int gl = act ? g : 0;  // idle threads shadow lane 0 (stores off)
+  double2* E = Ex + gl * PN;
+  const long ntiles = (F + 2 * PG - 1) / (2 * PG);
+  auto stage = [&](long tile) {
+    const long r0 = tile * 2 * PG;
+    const long nr = F - r0 < 2 * PG ? F - r0 : 2 * PG;
+    const int nd = (int)(nr * PN);
+    const double* src = in + r0 * PN;
+    for (int i = 2 * tid; i + 1 < nd; i += 2 * PTHREADS) cp_async16(S + i, src + i);
+    if ((nd & 1) && tid == 0) S[nd - 1] = src[nd - 1];
+  };
+  if (blockIdx.x < ntiles) stage(blockIdx.x);
+  cp_async_commit();
+  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long f = tile * 2 * PG + 2 * g;  // the lane's first row
+    const bool va = act && f < F, vb = act && f + 1 < F;
+    cp_async_wait<0>();
+    __syncthreads();
+    const int t = opaque(t0);
+    const double* ra = S + 2 * gl * PN;
+    pfa_dft(
+        E, t, act, [&](int n) { return va ? ra[n] : 0.0; }, [&](int n) { return vb ? ra[PN + n] : 0.0; },
+        [&] {  // S free: the next tile's rows stream in during the rest of the transform
+          if (tile + (long)gridDim.x < ntiles) stage(tile + gridDim.x);
+          cp_async_commit();
+        });
+    if (va) {
+      double* oa = out + f * PN;
+#pragma unroll 4
+      for (int m = 0; m < PB; ++m) {
+        const int k = t + PA * m;
+        const int km = k == 0 ? 0 : PN - k;
+        const double2 h = hartley_split(E[xslot(k)], E[xslot(km)]);
+        oa[k] = scale * h.x;
+        if (vb) oa[PN + k] = scale * h.y;
+      }
+    }
+  }
+}
+
+// Column pass along x1, in place on data[o][i][j] (n1 = 1023 rows of C
+// columns per slice): H1, divide by lam1[k] + lam2[j], H1.  Tile = 2G = 14
+// columns of one slice (the last tile of a slice may be narrower).
+constexpr int PW = 2 * PG;  // columns per tile
+
+__global__ void __launch_bounds__(PTHREADS, 1)
+    k_pfa_hcol(double* __restrict__ data, int nt, int C, const double* __restrict__ lam1,
+               const double* __restrict__ lam2) {
+  extern __shared__ double2 smem_raw[];
+  double* S = reinterpret_cast<double*>(smem_raw);  // [1023][PW]
+  double2* Ex = smem_raw + PG * PN;
+  pdl_trigger();
+  pdl_wait();
+  const int tid = threadIdx.x;
+  const int g = tid / PA, t0 = tid - g * PA;
+  const bool act = g < PG;
+  const int gl = act ? g : 0;  // idle threads shadow lane 0 (stores off)
+  double2* E = Ex + gl * PN;
+  const int ncb = (C + PW - 1) / PW;
+  const long ntiles = (long)nt * ncb;
+  auto stage = [&](long tile) {
+    const long o = tile / ncb;
+    const int c0 = (int)(tile - o * ncb) * PW;
+    const int nc = C - c0 < PW ? C - c0 : PW;
+    const double* src = data + o * PN * (long)C + c0;
+    for (int i = tid; i < PN * PW; i += PTHREADS) {
+      const int pos = i / PW, j = i - pos * PW;
+      if (j < nc) {
+        const unsigned d = (unsigned)__cvta_generic_to_shared(S + i);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src + (long)pos * C + j));
+      }
+    }
+  };
+  if (blockIdx.x < ntiles) stage(blockIdx.x);
+  cp_async_commit();
+  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long o = tile / ncb;
+    const int c0 = (int)(tile - o * ncb) * PW;
+    const int nc = C - c0 < PW ? C - c0 : PW;
+    const bool va = act && 2 * g < nc, vb = act && 2 * g + 1 < nc;
+    cp_async_wait<0>();
+    __syncthreads();
+    const int t = opaque(t0);
+    const double* sc = S + 2 * gl;
+    pfa_dft(
+        E, t, act, [&](int n) { return va ? sc[n * PW] : 0.0; }, [&](int n) { return vb ? sc[n * PW + 1] : 0.0; },
+        [&] {
+          if (tile + (long)gridDim.x < ntiles) stage(tile + gridDim.x);
+          cp_async_commit();
+        });
+    // Hartley split and the spectral division, positions k = t + 33 m
+    // (branch-free: idle threads compute on lane 0's slots, stores predicated)
+    double2 h[PB];
+    {
+      const int ca = c0 + 2 * gl;
+      const double l2a = __ldg(&lam2[ca]);
+      const double l2b = vb ? __ldg(&lam2[ca + 1]) : l2a;
+#pragma unroll
+      for (int m = 0; m < PB; ++m) {
+        const int k = t + PA * m;
+        const int km = k == 0 ? 0 : PN - k;
+        const double2 z = hartley_split(E[xslot(k)], E[xslot(km)]);
+        const double l1 = __ldg(&lam1[k]);
+        const double da = l1 + l2a, db = l1 + l2b;
+        const double inv = frcp(da * db);  // one reciprocal for both columns
+        h[m] = make_double2(z.x * (db * inv), vb ? z.y * (da * inv) : 0.0);
+      }
+    }
+    __syncthreads();  // mirror reads done
+#pragma unroll
+    for (int m = 0; m < PB; ++m)
+      if (act) E[t + PA * m] = h[m];
+    __syncthreads();
+    const double* Ed = reinterpret_cast<const double*>(E);
+    pfa_dft(
+        E, t, act, [&](int n) { return Ed[2 * n]; }, [&](int n) { return Ed[2 * n + 1]; }, [] {});
+    if (va) {
+      double* col = data + o * PN * (long)C + c0 + 2 * g;
+#pragma unroll 4
+      for (int m = 0; m < PB; ++m) {
+        const int k = t + PA * m;
+        const int km = k == 0 ? 0 : PN - k;
+        const double2 z = hartley_split(E[xslot(k)], E[xslot(km)]);
+        col[(long)k * C] = z.x;
+        if (vb) col[(long)k * C + 1] = z.y;
+      }
+    }
+    __syncthreads();  // E reads done before the next tile's pass A
+  }
+}
+
+}  // namespace
+
+bool pfa_supported(int n) { return n == PN; }
+
+cudaError_t launch_pfa_hrow(cudaStream_t st, LaunchCounter* lc, const double* in, double* out, long F,
+                            double scale) {
+  int cap = 0;
+  cudaError_t e = prep<k_pfa_hrow>(PSMEM, PTHREADS, cap);
+  if (e != cudaSuccess) return e;
+  count(lc);
+  const long tiles = (F + 2 * PG - 1) / (2 * PG);
+  return pdl_launch(PDL_PROW, k_pfa_hrow, clamp_grid(tiles, cap), PTHREADS, PSMEM, st, in, out, F, scale);
+}
+
+cudaError_t launch_pfa_hcol(cudaStream_t st, LaunchCounter* lc, double* data, int nt, int C, const double* lam1,
+                            const double* lam2) {
+  int cap = 0;
+  cudaError_t e = prep<k_pfa_hcol>(PSMEM, PTHREADS, cap);
+  if (e != cudaSuccess) return e;
+  count(lc);
+  const long tiles = (long)nt * ((C + PW - 1) / PW);
+  return pdl_launch(PDL_PCOL, k_pfa_hcol, clamp_grid(tiles, cap), PTHREADS, PSMEM, st, data, nt, C, lam1, lam2);
+}
+
+}  // namespace fdg

@@ -32,3 +32,28 @@ def test_c1_eigenvalues_real(ref):
         _, lam = ref.tchan(c, r)
         assert np.max(np.abs(lam.imag)) <= 1e-12 * np.max(np.abs(lam))
         assert np.allclose(lam.real[1:], lam.real[1:][::-1], rtol=1e-12, atol=0)
+
+
+def test_pfa_1023_index_maps():
+    """The Good-Thomas plan of csrc/fdg_pfa.cu, executed step for step in
+    numpy on one lane: pass-A gather x[(31 a + 33 b) mod 1023] -> DFT_31 ->
+    slot k2 * 33 + a; pass B DFT_33 as DFT_3 x DFT_11 over
+    a = (11 i + 3 j) mod 33 -> slot k2 * 33 + (22 c + 12 d) mod 33; X[k] read
+    back at (k mod 31) * 33 + k mod 33 equals the 1023-point DFT."""
+    N, PA, PB = 1023, 33, 31
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal(N) + 1j * rng.standard_normal(N)
+    E = np.zeros(N, complex)
+    for a in range(PA):
+        E[np.arange(PB) * PA + a] = np.fft.fft(x[(31 * a + 33 * np.arange(PB)) % N])
+    X2 = np.zeros(N, complex)
+    i, j = np.meshgrid(np.arange(3), np.arange(11), indexing="ij")
+    c, d = i, j
+    for t in range(PB):
+        r = E[t * PA + (11 * i + 3 * j) % PA]
+        r = np.fft.fft(np.fft.fft(r, axis=0), axis=1)
+        X2[t * PA + (22 * c + 12 * d) % PA] = r
+    k = np.arange(N)
+    X = X2[(k % PB) * PA + k % PA]
+    ref = np.fft.fft(x)
+    assert np.abs(X - ref).max() <= 1e-12 * np.abs(ref).max()
