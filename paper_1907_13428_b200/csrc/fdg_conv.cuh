@@ -103,7 +103,7 @@ struct SymTab {
   }
 };
 
-template <int L, bool SR, bool GT = false>
+template <int L, bool SR>
 struct CSmem {
   Ex ex;
   const double2* tw;
@@ -117,14 +117,6 @@ struct CSmem {
     ex.buf1 = base;
     ex.k = 0;
     double2* t = base + C::EXB;
-    if constexpr (GT) {  // tables read through L1 (lean column pass)
-      tw = gtw;
-      twist = gtwist;
-      sym.re = gsym_re;
-      sym.c = gsym;
-      stage = reinterpret_cast<double*>(t);
-      return;
-    }
     load_table(t, gtw, C::M);
     tw = t;
     t += C::M;
@@ -211,12 +203,12 @@ __device__ __forceinline__ void pair_sync(int g = 0) {
 #endif
 // The forward and the inverse transform share their per-thread twiddles
 // (TwCache) when the M-point transform has a single twiddled pass.
-template <int L, int LAYOUT, bool SR, bool NOCACHE = false>
+template <int L, int LAYOUT, bool SR>
 __device__ __forceinline__ void conv_half(double2 (&v)[CCfg<L>::R], Ex& ex, int t, int gs, int b,
                                           const double2* tw, const double2* twist, const SymTab<SR>& sym) {
   using C = CCfg<L>;
   constexpr int M = C::M, R = C::R, T = C::T, G2 = C::G2;
-  constexpr bool CACHE = FDG_TWCACHE && TwCache<M, R>::OK && !NOCACHE;
+  constexpr bool CACHE = FDG_TWCACHE && TwCache<M, R>::OK;
   if (b) {
 #pragma unroll
     for (int m = 0; m < R; ++m) v[m] = cmul(v[m], twist[t + T * m]);
@@ -484,29 +476,9 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
 }
 
 // ================================================================ columns
-// Lean S-mid column pass (FDG_K2_LEAN): tables read through L1, p and u
-// single-buffered (p's next tile staged once p is in registers, u's once the
-// first epilogue consumed it; the final epilogue re-reads p through L2), no
-// twiddle cache -> 3 CTAs (12 warps) per SM instead of 2.
-#ifndef FDG_K2_LEAN_MINB
-#define FDG_K2_LEAN_MINB 3
-#endif
-#ifndef FDG_K2_LEAN
-#define FDG_K2_LEAN 0
-#endif
-template <int L, int MODE>
-struct ColLean {
-  static constexpr bool value = FDG_K2_LEAN && L == 512 && MODE == 2;
-};
-template <int L, int MODE>
-struct ColMinB {
-  static constexpr int value = ColLean<L, MODE>::value ? FDG_K2_LEAN_MINB : CCfg<L>::MINB_COL;
-};
-
 template <int L, int MODE, bool PF, bool SR>
 struct ColCPlan {
   using C = CCfg<L>;
-  static constexpr bool LEAN = ColLean<L, MODE>::value && PF;
   // exchange layout: 1 = lane-major (sub-lane-local exchanges, __syncwarp),
   // else interleaved rows (CTA-wide barriers)
   static constexpr int LY = FDG_C_COLLY == 1 ? 1 : (C::HOMO_COL ? 2 : 0);
@@ -514,25 +486,23 @@ struct ColCPlan {
   static constexpr int P = LY == 1 ? W + 2 : W;   // staged row pitch (bank spread)
   static constexpr int TILE = PF ? C::M * P : 0;  // doubles per staged operand
   // MODE 2: double-buffered p (readable by both epilogues) and u
-  static constexpr int NST = MODE == 2 ? (LEAN ? 2 : 4) : 1;
-  static constexpr size_t SMEM =
-      LEAN ? sizeof(double2) * C::EXB + sizeof(double) * (size_t)TILE * NST : C::bytes((size_t)TILE * NST, SR);
+  static constexpr int NST = MODE == 2 ? 4 : 1;
+  static constexpr size_t SMEM = C::bytes((size_t)TILE * NST, SR);
 };
 
 // Column pass, modes as k_col (fdg_passes.cuh).  Interleaved exchange layout
 // (rows of G2 sub-lanes; split-interleaved when HOMO), sub-lanes of lane g
 // serve columns (2g, 2g+1) of the tile.
 template <int L, int MODE, bool PF, bool SR>
-__global__ void __launch_bounds__(CCfg<L>::THREADS, (ColMinB<L, MODE>::value)) k_colc(ColArgs a) {
+__global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(ColArgs a) {
   using Cf = CCfg<L>;
   static_assert(Cf::OK, "split pass configuration");
   constexpr int M = Cf::M, R = Cf::R, T = Cf::T, G = Cf::G, G2 = Cf::G2, HR = Cf::HR;
   using CP = ColCPlan<L, MODE, PF, SR>;
   constexpr int LY = CP::LY, W = CP::W, P = CP::P;
-  constexpr bool LEAN = CP::LEAN;
   extern __shared__ double2 smem_raw[];
   __shared__ double scratch[32];
-  CSmem<L, SR, LEAN> S(smem_raw, a.twh, a.twist, a.sym, a.sym_re);
+  CSmem<L, SR> S(smem_raw, a.twh, a.twist, a.sym, a.sym_re);
   pdl_trigger();
   pdl_wait();
   if (paused(a.guard)) return;
@@ -551,7 +521,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, (ColMinB<L, MODE>::value)) k
   if constexpr (PF) {
     if (blockIdx.x < ntiles) {
       stage_tile(S.stage, a.x, blockIdx.x);
-      if constexpr (MODE == 2) stage_tile(S.stage + (LEAN ? 1 : 2) * TILE, a.acc, blockIdx.x);
+      if constexpr (MODE == 2) stage_tile(S.stage + 2 * TILE, a.acc, blockIdx.x);
     }
     cp_async_commit();
   }
@@ -565,31 +535,18 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, (ColMinB<L, MODE>::value)) k
     const bool vb = PF || c + 1 < C;
     const size_t base = (size_t)o * n * C + c;
     const int nxt = tile + gridDim.x;
-    double* st_in = LEAN ? S.stage : S.stage + buf * TILE;
-    const double* st_u = LEAN ? S.stage + TILE : S.stage + (2 + buf) * TILE;  // MODE 2
+    double* st_in = S.stage + buf * TILE;
+    const double* st_u = S.stage + (2 + buf) * TILE;  // MODE 2
     double2 v[R];
     if constexpr (PF) {
       cp_async_wait<0>();
       __syncthreads();
 #pragma unroll
       for (int m = 0; m < R; ++m) v[m] = *reinterpret_cast<const double2*>(st_in + (t + m * T) * P + 2 * g);
-      if constexpr (LEAN) {
-        // a1 p^T p of the owned positions from the registers (p is not kept)
-        const double a1 = a.a1[o];
-#pragma unroll
-        for (int i = 0; i < HR; ++i) {
-          const double2 pv = b ? v[i + HR] : v[i];
-          e += a1 * pv.x * pv.x + a1 * pv.y * pv.y;
-        }
-      }
-      if constexpr (MODE != 2 || LEAN) __syncthreads();  // single input buffer
+      if constexpr (MODE != 2) __syncthreads();  // single input buffer
       if (nxt < ntiles) {
-        if constexpr (LEAN) {
-          stage_tile(S.stage, a.x, nxt);
-        } else {
-          stage_tile(S.stage + (buf ^ DB) * TILE, a.x, nxt);
-          if constexpr (MODE == 2) stage_tile(S.stage + (2 + (buf ^ 1)) * TILE, a.acc, nxt);
-        }
+        stage_tile(S.stage + (buf ^ DB) * TILE, a.x, nxt);
+        if constexpr (MODE == 2) stage_tile(S.stage + (2 + (buf ^ 1)) * TILE, a.acc, nxt);
       }
       cp_async_commit();
     } else {
@@ -599,7 +556,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, (ColMinB<L, MODE>::value)) k
         v[m] = (pos < n && vc) ? col_get<false>(a.x + base + (size_t)pos * C, C, c) : make_double2(0.0, 0.0);
       }
     }
-    conv_half<L, LY, SR, LEAN>(v, S.ex, t, mp.gs, b, S.tw, S.twist, S.sym);
+    conv_half<L, LY>(v, S.ex, t, mp.gs, b, S.tw, S.twist, S.sym);
     double2 y[HR];
     conv_combine<L, LY, !PF && MODE == 0>(v, y, S.ex, mp, S.twist);
 
@@ -623,16 +580,12 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, (ColMinB<L, MODE>::value)) k
         if (PF || (pos < n && vc)) {
           const size_t o2 = base + (size_t)pos * C;
           const double2 u = PF ? *reinterpret_cast<const double2*>(st_u + pos * P + 2 * g) : col_get<PF>(a.acc + o2, C, c);
+          const double2 pv = PF ? *reinterpret_cast<const double2*>(st_in + pos * P + 2 * g) : col_get<PF>(a.x + o2, C, c);
           const double bx = u.x + a.scale * y[i].x;
           const double by = u.y + a.scale * y[i].y;
           const double wx = bx * im2, wy = vb ? by * im2 : 0.0;
-          if constexpr (LEAN) {
-            e += wx * bx + wy * by;
-          } else {
-            const double2 pv = PF ? *reinterpret_cast<const double2*>(st_in + pos * P + 2 * g) : col_get<PF>(a.x + o2, C, c);
-            e += a1 * pv.x * pv.x + wx * bx;
-            if (vb) e += a1 * pv.y * pv.y + wy * by;
-          }
+          e += a1 * pv.x * pv.x + wx * bx;
+          if (vb) e += a1 * pv.y * pv.y + wy * by;
           col_put<PF>(a.w + o2, C, c, make_double2(wx, wy));
           y[i] = make_double2(wx, wy);
         } else {
@@ -642,10 +595,6 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, (ColMinB<L, MODE>::value)) k
       // both halves need all of w: each writes its positions into its own
       // slot column, then reads the lane's full column pair
       pair_sync<L, LY, Cf::HOMO_COL>();  // write-after-read: combine
-      if constexpr (LEAN) {  // u consumed: next tile's u into the single buffer
-        if (nxt < ntiles) stage_tile(S.stage + TILE, a.acc, nxt);
-        cp_async_commit();
-      }
       double2* sm = S.ex.next();
 #pragma unroll
       for (int i = 0; i < HR; ++i) sm[slot<LY, M, G2>(t + T * (i + b * HR), mp.gs)] = y[i];
@@ -658,25 +607,14 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, (ColMinB<L, MODE>::value)) k
       // only by its own half barrier (lane_sync), so a lagging half could
       // still be reading the slots the other half overwrites
       pair_sync<L, LY, Cf::HOMO_COL>();
-      conv_half<L, LY, SR, LEAN>(v, S.ex, t, mp.gs, b, S.tw, S.twist, S.sym);
-      // FDG_K2_LEAN == 1: p of the owned positions through L2, in flight
-      // during the combine (== 2: loaded in the epilogue)
-      constexpr bool PL = LEAN && FDG_K2_LEAN == 1;
-      double2 pl[PL ? HR : 1];
-      if constexpr (PL) {
-#pragma unroll
-        for (int i = 0; i < HR; ++i)
-          pl[i] = __ldg(reinterpret_cast<const double2*>(a.x + base + (size_t)(t + T * (i + b * HR)) * C));
-      }
+      conv_half<L, LY>(v, S.ex, t, mp.gs, b, S.tw, S.twist, S.sym);
       conv_combine<L, LY, !PF>(v, y, S.ex, mp, S.twist);
 #pragma unroll
       for (int i = 0; i < HR; ++i) {
         const int pos = t + T * (i + b * HR);
         if (!PF && (pos >= n || !vc)) continue;
         const size_t o2 = base + (size_t)pos * C;
-        const double2 pv = PL     ? pl[i]
-                           : LEAN ? __ldg(reinterpret_cast<const double2*>(a.x + o2))
-                                  : (PF ? *reinterpret_cast<const double2*>(st_in + pos * P + 2 * g) : col_get<PF>(a.x + o2, C, c));
+        const double2 pv = PF ? *reinterpret_cast<const double2*>(st_in + pos * P + 2 * g) : col_get<PF>(a.x + o2, C, c);
         col_put<PF>(a.out + o2, C, c, make_double2(a.scale * y[i].x + a1 * pv.x, a.scale * y[i].y + a1 * pv.y));
       }
     }
