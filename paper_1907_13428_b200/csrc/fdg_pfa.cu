@@ -40,9 +40,20 @@ namespace {
 constexpr int PN = 1023;     // transform length
 constexpr int PA = 33;       // outer factor (3 x 11), threads per lane
 constexpr int PB = 31;       // inner factor
-constexpr int PG = 7;        // lanes per CTA
-constexpr int PTHREADS = 256;
-constexpr size_t PSMEM = 2 * (size_t)PG * PN * sizeof(double2);
+constexpr int PH = 16;       // mirror-pair rounds: k = t + 33 m < 512 for m < 16
+// lanes per CTA of the row / column passes (G lanes = 33 G working threads)
+#ifndef FDG_PFA_GROW
+#define FDG_PFA_GROW 7
+#endif
+#ifndef FDG_PFA_GCOL
+#define FDG_PFA_GCOL 7
+#endif
+template <int G>
+struct PCfg {
+  static constexpr int THREADS = (PA * G + 31) / 32 * 32;
+  static constexpr size_t SMEM = 2 * (size_t)G * PN * sizeof(double2);  // staging + exchange
+  static constexpr int MINB = SMEM <= 113 * 1024 ? 2 : 1;
+};
 
 // cos / sin (2 pi j / P), j < P (fdg_pfa_tab.h, scripts/gen_pfa_consts.py)
 __constant__ double kC3[3] = FDG_PFA_C3;
@@ -89,43 +100,64 @@ __device__ __forceinline__ void dft_odd(const double2 (&x)[P], Put&& put) {
   for (int k = 0; k < H; ++k) sum = cadd(sum, s[k]);
   put(0, sum);
   if constexpr (P == 31) {
-#pragma unroll 1
-    for (int m = 1; m <= H; ++m) {
+    // outputs m and m + 8 per iteration: 8 independent accumulation chains
+    auto one = [&](int m, double2& A, double2& B) {
       const double c0 = kT31.c[m - 1][0], s0 = kT31.s[m - 1][0];
-      double2 A = make_double2(fma(c0, s[0].x, x0.x), fma(c0, s[0].y, x0.y));
-      double2 B = make_double2(s0 * d[0].x, s0 * d[0].y);
+      A = make_double2(fma(c0, s[0].x, x0.x), fma(c0, s[0].y, x0.y));
+      B = make_double2(s0 * d[0].x, s0 * d[0].y);
+    };
+    auto step = [&](int m, int k, double2& A, double2& B) {
+      const double c = kT31.c[m - 1][k - 1], sn = kT31.s[m - 1][k - 1];
+      A.x = fma(c, s[k - 1].x, A.x);
+      A.y = fma(c, s[k - 1].y, A.y);
+      B.x = fma(sn, d[k - 1].x, B.x);
+      B.y = fma(sn, d[k - 1].y, B.y);
+    };
+    auto out = [&](int m, const double2& A, const double2& B) {
+      put(m, make_double2(A.x + B.y, A.y - B.x));
+      put(P - m, make_double2(A.x - B.y, A.y + B.x));
+    };
+#pragma unroll 1
+    for (int m = 1; m <= 7; ++m) {
+      double2 A, B, A2, B2;
+      one(m, A, B);
+      one(m + 8, A2, B2);
 #pragma unroll
       for (int k = 2; k <= H; ++k) {
-        const double c = kT31.c[m - 1][k - 1], sn = kT31.s[m - 1][k - 1];
+        step(m, k, A, B);
+        step(m + 8, k, A2, B2);
+      }
+      out(m, A, B);
+      out(m + 8, A2, B2);
+    }
+    {
+      double2 A, B;
+      one(8, A, B);
+#pragma unroll
+      for (int k = 2; k <= H; ++k) step(8, k, A, B);
+      out(8, A, B);
+    }
+  } else {
+#pragma unroll
+    for (int m = 1; m <= H; ++m) {
+      double2 A = x0, B;
+#pragma unroll
+      for (int k = 1; k <= H; ++k) {
+        const int j = (k * m) % P;
+        const double c = twc<P>(j), sn = tws<P>(j);
         A.x = fma(c, s[k - 1].x, A.x);
         A.y = fma(c, s[k - 1].y, A.y);
-        B.x = fma(sn, d[k - 1].x, B.x);
-        B.y = fma(sn, d[k - 1].y, B.y);
+        if (k == 1) {
+          B = make_double2(sn * d[0].x, sn * d[0].y);
+        } else {
+          B.x = fma(sn, d[k - 1].x, B.x);
+          B.y = fma(sn, d[k - 1].y, B.y);
+        }
       }
+      // outputs leave as soon as they are formed (the inputs stay live)
       put(m, make_double2(A.x + B.y, A.y - B.x));
       put(P - m, make_double2(A.x - B.y, A.y + B.x));
     }
-    return;
-  }
-#pragma unroll
-  for (int m = 1; m <= H; ++m) {
-    double2 A = x0, B;
-#pragma unroll
-    for (int k = 1; k <= H; ++k) {
-      const int j = (k * m) % P;
-      const double c = twc<P>(j), sn = tws<P>(j);
-      A.x = fma(c, s[k - 1].x, A.x);
-      A.y = fma(c, s[k - 1].y, A.y);
-      if (k == 1) {
-        B = make_double2(sn * d[0].x, sn * d[0].y);
-      } else {
-        B.x = fma(sn, d[k - 1].x, B.x);
-        B.y = fma(sn, d[k - 1].y, B.y);
-      }
-    }
-    // outputs leave as soon as they are formed (the inputs stay live)
-    put(m, make_double2(A.x + B.y, A.y - B.x));
-    put(P - m, make_double2(A.x - B.y, A.y + B.x));
   }
 }
 
@@ -138,35 +170,44 @@ __device__ __forceinline__ int opaque(int v) {
   return r;
 }
 
-// Slot of X[k] in the exchange area after pfa_dft (CRT order).
-__device__ __forceinline__ int xslot(int k) { return (k % PB) * PA + k % PA; }
-
-// Pass-A gather of one real fibre: v[b] = x[(31 a + 33 b) mod 1023], a = t.
-template <class F>
-__device__ __forceinline__ void pfa_gather(double (&v)[PB], int t, F&& src) {
-  int idx = 31 * t;
-#pragma unroll
-  for (int b = 0; b < PB; ++b) {
-    v[b] = src(idx);
-    idx += 33;
-    if (idx >= PN) idx -= PN;
+// Slot of X[k] in the exchange area after pfa_dft (CRT order): k mod 31
+// rows of 33, k mod 33 within the row.  MirrorSlots walks the slots of
+// k = t + 33 m and of its mirror 1023 - k for m = 0, 1, ... incrementally
+// (k mod 33 = t, k mod 31 = (t + 2 m) mod 31).
+struct MirrorSlots {
+  int q, ta, tb;
+  __device__ __forceinline__ explicit MirrorSlots(int t) : q(t % PB), ta(t), tb(t == 0 ? 0 : PA - t) {}
+  __device__ __forceinline__ int k() const { return q * PA + ta; }
+  __device__ __forceinline__ int km() const { return (q == 0 ? 0 : PB - q) * PA + tb; }
+  __device__ __forceinline__ void next() {
+    q += 2;
+    if (q >= PB) q -= PB;
   }
-}
+};
 
-// The lane's DFT of x = xa + i xb (two real fibres read by srca / srcb(n))
+// The lane's DFT of x = xa + i xb (two real fibres, src(n) = (xa[n], xb[n]))
 // into the lane's exchange area E (1023 double2), X[k] at E[xslot(k)].
 // Every thread of the CTA calls it (CTA barriers inside); `act`: the thread
 // serves a lane (thread a = t < 33 of pass A, k2 = t < 31 of pass B).
 // `freed()` runs once every gather is done (the source area may be reused;
 // E is written only after it).
-template <class FA, class FB, class FR>
-__device__ __forceinline__ void pfa_dft(double2* E, int t, bool act, FA&& srca, FB&& srcb, FR&& freed) {
+template <class FS, class FR>
+__device__ __forceinline__ void pfa_dft(double2* E, int t, bool act, FS&& src, FR&& freed) {
   // Idle threads (no lane, or t >= 31 in pass B) run the same code on valid
   // addresses with their stores predicated off: branch-free blocks keep
   // ptxas' register allocation spill-free.
   double va[PB], vb[PB];
-  pfa_gather(va, t, srca);
-  pfa_gather(vb, t, srcb);
+  {
+    int idx = 31 * t;  // (31 a + 33 b) mod 1023, a = t
+#pragma unroll
+    for (int b = 0; b < PB; ++b) {
+      const double2 z = src(idx);
+      va[b] = z.x;
+      vb[b] = z.y;
+      idx += 33;
+      if (idx >= PN) idx -= PN;
+    }
+  }
   __syncthreads();
   freed();
   {
@@ -203,8 +244,10 @@ __device__ __forceinline__ void pfa_dft(double2* E, int t, bool act, FA&& srca, 
 }
 
 // Row pass along x2 (rows of 1023 contiguous doubles): out = scale * H2 in.
-__global__ void __launch_bounds__(PTHREADS, 1)
+template <int PG>
+__global__ void __launch_bounds__(PCfg<PG>::THREADS, PCfg<PG>::MINB)
     k_pfa_hrow(const double* __restrict__ in, double* __restrict__ out, long F, double scale) {
+  constexpr int PTHREADS = PCfg<PG>::THREADS;
   extern __shared__ double2 smem_raw[];
   double* S = reinterpret_cast<double*>(smem_raw);  // 2G fibres of the tile
   double2* Ex = smem_raw + PG * PN;                  // G lanes
@@ -234,20 +277,29 @@ __global__ void __launch_bounds__(PTHREADS, 1)
     const int t = opaque(t0);
     const double* ra = S + 2 * gl * PN;
     pfa_dft(
-        E, t, act, [&](int n) { return va ? ra[n] : 0.0; }, [&](int n) { return vb ? ra[PN + n] : 0.0; },
+        E, t, act, [&](int n) { return make_double2(va ? ra[n] : 0.0, vb ? ra[PN + n] : 0.0); },
         [&] {  // S free: the next tile's rows stream in during the rest of the transform
           if (tile + (long)gridDim.x < ntiles) stage(tile + gridDim.x);
           cp_async_commit();
         });
     if (va) {
       double* oa = out + f * PN;
+      // mirror pairs (k, 1023 - k), k = t + 33 m < 512: each X read once
+      MirrorSlots ms(t);
 #pragma unroll 4
-      for (int m = 0; m < PB; ++m) {
+      for (int m = 0; m < PH; ++m, ms.next()) {
         const int k = t + PA * m;
-        const int km = k == 0 ? 0 : PN - k;
-        const double2 h = hartley_split(E[xslot(k)], E[xslot(km)]);
-        oa[k] = scale * h.x;
-        if (vb) oa[PN + k] = scale * h.y;
+        if (k < PN / 2 + 1) {
+          const double2 zk = E[ms.k()], zm = E[ms.km()];
+          const double2 h = hartley_split(zk, zm);
+          oa[k] = scale * h.x;
+          if (vb) oa[PN + k] = scale * h.y;
+          if (k) {
+            const double2 hm = hartley_split(zm, zk);
+            oa[PN - k] = scale * hm.x;
+            if (vb) oa[2 * PN - k] = scale * hm.y;
+          }
+        }
       }
     }
   }
@@ -256,11 +308,12 @@ __global__ void __launch_bounds__(PTHREADS, 1)
 // Column pass along x1, in place on data[o][i][j] (n1 = 1023 rows of C
 // columns per slice): H1, divide by lam1[k] + lam2[j], H1.  Tile = 2G = 14
 // columns of one slice (the last tile of a slice may be narrower).
-constexpr int PW = 2 * PG;  // columns per tile
-
-__global__ void __launch_bounds__(PTHREADS, 1)
+template <int PG>
+__global__ void __launch_bounds__(PCfg<PG>::THREADS, PCfg<PG>::MINB)
     k_pfa_hcol(double* __restrict__ data, int nt, int C, const double* __restrict__ lam1,
                const double* __restrict__ lam2) {
+  constexpr int PTHREADS = PCfg<PG>::THREADS;
+  constexpr int PW = 2 * PG;  // columns per tile
   extern __shared__ double2 smem_raw[];
   double* S = reinterpret_cast<double*>(smem_raw);  // [1023][PW]
   double2* Ex = smem_raw + PG * PN;
@@ -298,46 +351,74 @@ __global__ void __launch_bounds__(PTHREADS, 1)
     const int t = opaque(t0);
     const double* sc = S + 2 * gl;
     pfa_dft(
-        E, t, act, [&](int n) { return va ? sc[n * PW] : 0.0; }, [&](int n) { return vb ? sc[n * PW + 1] : 0.0; },
-        [&] {
-          if (tile + (long)gridDim.x < ntiles) stage(tile + gridDim.x);
-          cp_async_commit();
-        });
-    // Hartley split and the spectral division, positions k = t + 33 m
+        E, t, act,
+        [&](int n) {
+          const double2 z = *reinterpret_cast<const double2*>(sc + n * PW);
+          return make_double2(va ? z.x : 0.0, vb ? z.y : 0.0);
+        },
+        [] {});
+    // Hartley split and the spectral division, positions k = t + 33 m, into
+    // the staging area (free once the gathers are done: the next tile is
+    // staged only after the second transform's gathers)
     // (branch-free: idle threads compute on lane 0's slots, stores predicated)
-    double2 h[PB];
+    double2* Sh = reinterpret_cast<double2*>(S) + gl * PN;
     {
       const int ca = c0 + 2 * gl;
       const double l2a = __ldg(&lam2[ca]);
       const double l2b = vb ? __ldg(&lam2[ca + 1]) : l2a;
-#pragma unroll
-      for (int m = 0; m < PB; ++m) {
-        const int k = t + PA * m;
-        const int km = k == 0 ? 0 : PN - k;
-        const double2 z = hartley_split(E[xslot(k)], E[xslot(km)]);
+      auto divide = [&](double2 z, int k) {
         const double l1 = __ldg(&lam1[k]);
         const double da = l1 + l2a, db = l1 + l2b;
         const double inv = frcp(da * db);  // one reciprocal for both columns
-        h[m] = make_double2(z.x * (db * inv), vb ? z.y * (da * inv) : 0.0);
+        if (act) Sh[k] = make_double2(z.x * (db * inv), vb ? z.y * (da * inv) : 0.0);
+      };
+      MirrorSlots ms(t);
+#pragma unroll
+      for (int m = 0; m < PH; ++m, ms.next()) {
+        const int k = t + PA * m;
+        if (k < PN / 2 + 1) {  // mirror pair (k, 1023 - k)
+          const double2 zk = E[ms.k()], zm = E[ms.km()];
+          divide(hartley_split(zk, zm), k);
+          if (k) divide(hartley_split(zm, zk), PN - k);
+        }
+      }
+    }
+    __syncthreads();  // every value of the divided spectrum in Sh
+    pfa_dft(E, t, act, [&](int n) { return Sh[n]; },
+            [&] {  // staging area free: the next tile streams in during the rest
+              if (tile + (long)gridDim.x < ntiles) stage(tile + gridDim.x);
+              cp_async_commit();
+            });
+    // Hartley split into registers (mirror pairs, each X read once), then
+    // the tile goes out through the exchange area as [pos][PW] rows (8-byte
+    // stores of whole row segments; storing the lanes' columns directly
+    // scatters every warp store over 32 rows)
+    double2 h[PH], hm[PH];
+    {
+      MirrorSlots ms(t);
+#pragma unroll
+      for (int m = 0; m < PH; ++m, ms.next()) {
+        const double2 zk = E[ms.k()], zm = E[ms.km()];  // (m = 15, t > 16: unused)
+        h[m] = hartley_split(zk, zm);
+        hm[m] = hartley_split(zm, zk);
       }
     }
     __syncthreads();  // mirror reads done
+    double* Et = reinterpret_cast<double*>(Ex);  // [1023][PW] (G lanes x 1023 double2 = 1023 x PW doubles)
 #pragma unroll
-    for (int m = 0; m < PB; ++m)
-      if (act) E[t + PA * m] = h[m];
+    for (int m = 0; m < PH; ++m) {
+      const int k = t + PA * m;
+      if (act && k < PN / 2 + 1) {
+        *reinterpret_cast<double2*>(Et + k * PW + 2 * g) = h[m];
+        if (k) *reinterpret_cast<double2*>(Et + (PN - k) * PW + 2 * g) = hm[m];
+      }
+    }
     __syncthreads();
-    const double* Ed = reinterpret_cast<const double*>(E);
-    pfa_dft(
-        E, t, act, [&](int n) { return Ed[2 * n]; }, [&](int n) { return Ed[2 * n + 1]; }, [] {});
-    if (va) {
-      double* col = data + o * PN * (long)C + c0 + 2 * g;
-#pragma unroll 4
-      for (int m = 0; m < PB; ++m) {
-        const int k = t + PA * m;
-        const int km = k == 0 ? 0 : PN - k;
-        const double2 z = hartley_split(E[xslot(k)], E[xslot(km)]);
-        col[(long)k * C] = z.x;
-        if (vb) col[(long)k * C + 1] = z.y;
+    {
+      double* dst = data + o * PN * (long)C + c0;
+      for (int i = tid; i < PN * PW; i += PTHREADS) {
+        const int pos = i / PW, j = i - pos * PW;
+        if (j < nc) dst[(long)pos * C + j] = Et[i];
       }
     }
     __syncthreads();  // E reads done before the next tile's pass A
@@ -350,22 +431,26 @@ bool pfa_supported(int n) { return n == PN; }
 
 cudaError_t launch_pfa_hrow(cudaStream_t st, LaunchCounter* lc, const double* in, double* out, long F,
                             double scale) {
+  using Cf = PCfg<FDG_PFA_GROW>;
   int cap = 0;
-  cudaError_t e = prep<k_pfa_hrow>(PSMEM, PTHREADS, cap);
+  cudaError_t e = prep<k_pfa_hrow<FDG_PFA_GROW>>(Cf::SMEM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
   count(lc);
-  const long tiles = (F + 2 * PG - 1) / (2 * PG);
-  return pdl_launch(PDL_PROW, k_pfa_hrow, clamp_grid(tiles, cap), PTHREADS, PSMEM, st, in, out, F, scale);
+  const long tiles = (F + 2 * FDG_PFA_GROW - 1) / (2 * FDG_PFA_GROW);
+  return pdl_launch(PDL_PROW, k_pfa_hrow<FDG_PFA_GROW>, clamp_grid(tiles, cap), Cf::THREADS, Cf::SMEM, st, in,
+                    out, F, scale);
 }
 
 cudaError_t launch_pfa_hcol(cudaStream_t st, LaunchCounter* lc, double* data, int nt, int C, const double* lam1,
                             const double* lam2) {
+  using Cf = PCfg<FDG_PFA_GCOL>;
   int cap = 0;
-  cudaError_t e = prep<k_pfa_hcol>(PSMEM, PTHREADS, cap);
+  cudaError_t e = prep<k_pfa_hcol<FDG_PFA_GCOL>>(Cf::SMEM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
   count(lc);
-  const long tiles = (long)nt * ((C + PW - 1) / PW);
-  return pdl_launch(PDL_PCOL, k_pfa_hcol, clamp_grid(tiles, cap), PTHREADS, PSMEM, st, data, nt, C, lam1, lam2);
+  const long tiles = (long)nt * ((C + 2 * FDG_PFA_GCOL - 1) / (2 * FDG_PFA_GCOL));
+  return pdl_launch(PDL_PCOL, k_pfa_hcol<FDG_PFA_GCOL>, clamp_grid(tiles, cap), Cf::THREADS, Cf::SMEM, st, data,
+                    nt, C, lam1, lam2);
 }
 
 }  // namespace fdg

@@ -14,7 +14,9 @@ from collections import OrderedDict
 
 # algorithmic N-vector passes per launch (SURVEY.md 8d / DESIGN.md)
 ALG = {"K1_row_p_update_B": 6, "K2_col_S_mid": 4, "K3_row_BT_update": 4, "P1_hartley_x2": 2,
-       "P2_hartley_x1": 2, "P3_t_filter": 2, "P4_hartley_x1": 2, "P5_hartley_x2_dot": 3, "X_axpy": 3}
+       "P2_hartley_x1": 2, "P3_t_filter": 2, "P4_hartley_x1": 2, "P5_hartley_x2_dot": 3, "X_axpy": 3,
+       # BASELINE C1: matvec row (2N) + column-with-accumulate (3N); 2-level solve 3 x 2N
+       "row_apply": 2, "col_acc": 3, "C1_pfa_x2": 2, "C1_pfa_x1": 2}
 
 
 def pass_name(kernel, seen):
@@ -33,6 +35,10 @@ def pass_name(kernel, seen):
         return "P2_hartley_x1" if seen["hc"] % 2 == 1 else "P4_hartley_x1"
     if "k_axpy_dev" in k:
         return "X_axpy"
+    if "k_pfa_hrow" in k:
+        return "C1_pfa_x2"
+    if "k_pfa_hcol" in k:
+        return "C1_pfa_x1"
     return k.replace("void ", "")
 
 
@@ -126,8 +132,39 @@ def launches(log, out_csv, cmd):
     print(open(out_csv).read())
 
 
+STALLS = ["wait", "short_scoreboard", "long_scoreboard", "barrier", "mio_throttle", "math_pipe_throttle",
+          "not_selected", "selected", "no_instruction", "lg_throttle", "branch_resolving", "dispatch_stall",
+          "drain", "membar", "sleeping", "tex_throttle", "imc_miss", "misc"]
+
+
+def stalls(rep, out_txt, label):
+    """Top-8 warp stall reasons per issued instruction for every kernel of a capture."""
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, data = rows[0], rows[2:]
+    ix = {h: i for i, h in enumerate(hdr)}
+    seen = {}
+    with open(out_txt, "w") as fh:
+        fh.write(f"# warp stall breakdown per issued instruction (smsp__average_warps_issue_stalled_*_per_issue_active.ratio)\n")
+        fh.write(f"# {label}: {rep.split('/')[-1]}; top 8 reasons per kernel\n")
+        for r in data:
+            name = pass_name(r[ix["Kernel Name"]], seen)
+            kern = r[ix["Kernel Name"]].split("(")[0].replace("void ", "").replace("fdg::", "")
+            us = f(r[ix["gpu__time_duration.sum"]]) if "gpu__time_duration.sum" in ix else float("nan")
+            vals = []
+            for st in STALLS:
+                m = f"smsp__average_warps_issue_stalled_{st}_per_issue_active.ratio"
+                if m in ix:
+                    vals.append((f(r[ix[m]]), st))
+            vals.sort(reverse=True)
+            fh.write(f"{name:22s} {kern[:40]:40s} time={us:10.1f} " + " ".join(f"{st}={v:.2f}" for v, st in vals[:8]) + "\n")
+    print(open(out_txt).read())
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "full":
         full(*sys.argv[2:7])
+    elif sys.argv[1] == "stalls":
+        stalls(*sys.argv[2:5])
     else:
         launches(*sys.argv[2:5])
