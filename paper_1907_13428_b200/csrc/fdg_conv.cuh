@@ -57,6 +57,9 @@ namespace fdg {
 #ifndef FDG_C_COLLY
 #define FDG_C_COLLY 2
 #endif
+#ifndef FDG_K2_EREG
+#define FDG_K2_EREG 1  // S-mid column pass: a1 p^T p from the input registers
+#endif
 
 template <int L>
 struct CCfg {
@@ -543,6 +546,16 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
       __syncthreads();
 #pragma unroll
       for (int m = 0; m < R; ++m) v[m] = *reinterpret_cast<const double2*>(st_in + (t + m * T) * P + 2 * g);
+      if constexpr (MODE == 2 && FDG_K2_EREG) {
+        // a1 p^T p of the owned positions from the registers (saves the
+        // staged re-read of p in the first epilogue)
+        const double a1 = a.a1[o];
+#pragma unroll
+        for (int i = 0; i < HR; ++i) {
+          const double2 pv = b ? v[i + HR] : v[i];
+          e = fma(a1, fma(pv.x, pv.x, pv.y * pv.y), e);
+        }
+      }
       if constexpr (MODE != 2) __syncthreads();  // single input buffer
       if (nxt < ntiles) {
         stage_tile(S.stage + (buf ^ DB) * TILE, a.x, nxt);
@@ -580,12 +593,16 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
         if (PF || (pos < n && vc)) {
           const size_t o2 = base + (size_t)pos * C;
           const double2 u = PF ? *reinterpret_cast<const double2*>(st_u + pos * P + 2 * g) : col_get<PF>(a.acc + o2, C, c);
-          const double2 pv = PF ? *reinterpret_cast<const double2*>(st_in + pos * P + 2 * g) : col_get<PF>(a.x + o2, C, c);
           const double bx = u.x + a.scale * y[i].x;
           const double by = u.y + a.scale * y[i].y;
           const double wx = bx * im2, wy = vb ? by * im2 : 0.0;
-          e += a1 * pv.x * pv.x + wx * bx;
-          if (vb) e += a1 * pv.y * pv.y + wy * by;
+          if (PF && FDG_K2_EREG) {
+            e += wx * bx + wy * by;
+          } else {
+            const double2 pv = PF ? *reinterpret_cast<const double2*>(st_in + pos * P + 2 * g) : col_get<PF>(a.x + o2, C, c);
+            e += a1 * pv.x * pv.x + wx * bx;
+            if (vb) e += a1 * pv.y * pv.y + wy * by;
+          }
           col_put<PF>(a.w + o2, C, c, make_double2(wx, wy));
           y[i] = make_double2(wx, wy);
         } else {
