@@ -1357,6 +1357,12 @@ fdg_pc_s* make_pc2(fdg_ctx ctx, int nt, int n1, int n2, const double* l1, const 
     }
     if (im > 1e-10 * std::max(mx, 1e-300))
       fail(FDG_EUNSUPPORTED, "fdg: 2-level preconditioner needs real eigenvalues (symmetric factors)");
+    // the Hartley formulation (and the PFA passes' mirror-pair lambda) needs
+    // lam[k] == lam[n - k] (real symmetric circulant)
+    double odd = 0.0;
+    for (int i = 1; i < n; ++i) odd = std::max(odd, std::abs(lam[2 * i] - lam[2 * (n - i)]));
+    if (odd > 1e-10 * std::max(mx, 1e-300))
+      fail(FDG_EUNSUPPORTED, "fdg: 2-level preconditioner needs even eigenvalues (symmetric factors)");
   }
   auto pc = std::make_unique<fdg_pc_s>();
   pc->ctx = ctx;

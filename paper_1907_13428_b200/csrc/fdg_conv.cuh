@@ -57,6 +57,13 @@ namespace fdg {
 #ifndef FDG_C_COLLY
 #define FDG_C_COLLY 2
 #endif
+#ifndef FDG_TMA_ROWS
+#define FDG_TMA_ROWS 1  // staged split row passes: bulk-copy (TMA) staging with mbarriers
+#endif
+#ifndef FDG_TMA_COLS
+#define FDG_TMA_COLS 2  // staged split column passes: 2 = 2-D tensor-map TMA boxes, 1 = one bulk copy per
+                        // row segment (C2 K2 237 -> 555 us), 0 = per-thread cp.async
+#endif
 #ifndef FDG_K2_EREG
 #define FDG_K2_EREG 1  // S-mid column pass: a1 p^T p from the input registers
 #endif
@@ -287,7 +294,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
   constexpr int M = C::M, R = C::R, T = C::T, G = C::G, HR = C::HR;
   constexpr int TILE = RP::TILE;
   constexpr bool SEPI = RP::SEPI;
-  extern __shared__ double2 smem_raw[];
+  extern __shared__ __align__(128) double2 smem_raw[];
   __shared__ double scratch[32];
   CSmem<L, SR> S(smem_raw, a.twh, a.twist, a.sym, a.sym_re);
   pdl_trigger();
@@ -331,7 +338,26 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
       xpre[i] = make_double2(a.xs[rx + pos], a.xs[rx + n + pos]);
     }
   };
-  if constexpr (PF) {
+  // TMA staging: barrier 0 = the tile's FFT input, 1 = its epilogue operands
+  constexpr bool TMA = PF && FDG_TMA_ROWS;
+  __shared__ alignas(8) unsigned long long bars[2];
+  constexpr unsigned TB = sizeof(double) * TILE;  // bytes per staged operand
+  unsigned ph_in = 0, ph_ep = 0;
+  auto stage_in = [&](int tl) {  // elected thread: next FFT input (+ d_old)
+    const unsigned nb = (MODE == 2 && !first) ? 2 * TB : TB;
+    mbar_expect_tx(&bars[0], nb);
+    bulk_g2s(st_in, in0 + (size_t)tl * 2 * G * n, TB, &bars[0]);
+    if (MODE == 2 && !first) bulk_g2s(st_in2, in1 + (size_t)tl * 2 * G * n, TB, &bars[0]);
+  };
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      mbar_init_fence();
+      if (blockIdx.x < ntiles) stage_in(blockIdx.x);
+    }
+    if (upd_x && blockIdx.x < ntiles) load_x(blockIdx.x);
+  } else if constexpr (PF) {
     if (blockIdx.x < ntiles) {
       stage_rows(st_in, in0 + (size_t)blockIdx.x * 2 * G * n, TILE);
       if (MODE == 2 && !first) stage_rows(st_in2, in1 + (size_t)blockIdx.x * 2 * G * n, TILE);
@@ -339,7 +365,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
     }
     cp_async_commit();
   }
-  __syncthreads();  // tables
+  __syncthreads();  // tables (and the barriers' initialization)
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int f0 = tile * 2 * G;
     const int f = f0 + 2 * g;
@@ -347,9 +373,15 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
     const size_t ra = (size_t)f * n;
     double2 v[R];
     bool tile_nb = false;
+    bool ep_armed = false;
     if constexpr (PF) {
-      cp_async_wait<0>();
-      __syncthreads();
+      if constexpr (TMA) {
+        mbar_wait(&bars[0], ph_in);
+        ph_in ^= 1;
+      } else {
+        cp_async_wait<0>();
+        __syncthreads();
+      }
 #pragma unroll
       for (int m = 0; m < R; ++m) {
         const int pos = t + m * T;
@@ -381,23 +413,50 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
       __syncthreads();  // st_in and the epilogue staging are free
       const int k = f0 / a.n1;
       tile_nb = a.tkind == 1 && (a.tdir < 0 ? k >= 1 : k + 1 < a.nt);
-      if constexpr (SEPI) {
-        if (tile_nb) {
-          stage_rows(st_nb, in0 + (size_t)f0 * n + noff, TILE);
-          if (MODE == 2 && !first) stage_rows(st_nb2, in1 + (size_t)f0 * n + noff, TILE);
-        }
-        if constexpr (MODE == 1) {
-          stage_rows(st_vp, a.vp + (size_t)f0 * n, TILE);
-          if (a.r) stage_rows(st_r, (a.r_in ? a.r_in : a.r) + (size_t)f0 * n, TILE);
-        }
-      }
-      cp_async_commit();  // group E
       const int nxt = tile + gridDim.x;
-      if (nxt < ntiles) {
-        stage_rows(st_in, in0 + (size_t)nxt * 2 * G * n, TILE);
-        if (MODE == 2 && !first) stage_rows(st_in2, in1 + (size_t)nxt * 2 * G * n, TILE);
+      if constexpr (TMA) {
+        // epilogue operands of this tile, then the next tile's input
+        unsigned eb = 0;
+        if constexpr (SEPI) {
+          if (tile_nb) eb += (MODE == 2 && !first) ? 2 * TB : TB;
+          if constexpr (MODE == 1) eb += a.r ? 2 * TB : TB;
+        }
+        ep_armed = eb != 0;
+        if (threadIdx.x == 0) {
+          fence_proxy_async();  // the reads of st_in / the previous epilogue before the refill
+          if (ep_armed) {
+            mbar_expect_tx(&bars[1], eb);
+            if constexpr (SEPI) {
+              if (tile_nb) {
+                bulk_g2s(st_nb, in0 + (size_t)f0 * n + noff, TB, &bars[1]);
+                if (MODE == 2 && !first) bulk_g2s(st_nb2, in1 + (size_t)f0 * n + noff, TB, &bars[1]);
+              }
+              if constexpr (MODE == 1) {
+                bulk_g2s(st_vp, a.vp + (size_t)f0 * n, TB, &bars[1]);
+                if (a.r) bulk_g2s(st_r, (a.r_in ? a.r_in : a.r) + (size_t)f0 * n, TB, &bars[1]);
+              }
+            }
+          }
+          if (nxt < ntiles) stage_in(nxt);
+        }
+      } else {
+        if constexpr (SEPI) {
+          if (tile_nb) {
+            stage_rows(st_nb, in0 + (size_t)f0 * n + noff, TILE);
+            if (MODE == 2 && !first) stage_rows(st_nb2, in1 + (size_t)f0 * n + noff, TILE);
+          }
+          if constexpr (MODE == 1) {
+            stage_rows(st_vp, a.vp + (size_t)f0 * n, TILE);
+            if (a.r) stage_rows(st_r, (a.r_in ? a.r_in : a.r) + (size_t)f0 * n, TILE);
+          }
+        }
+        cp_async_commit();  // group E
+        if (nxt < ntiles) {
+          stage_rows(st_in, in0 + (size_t)nxt * 2 * G * n, TILE);
+          if (MODE == 2 && !first) stage_rows(st_in2, in1 + (size_t)nxt * 2 * G * n, TILE);
+        }
+        cp_async_commit();  // group I
       }
-      cp_async_commit();  // group I
     } else {
 #pragma unroll
       for (int m = 0; m < R; ++m) {
@@ -425,8 +484,15 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_ROW) k_rowc(Ro
     conv_combine<L, 1, !PF>(v, y, S.ex, mp, S.twist);
 
     if constexpr (SEPI) {
-      cp_async_wait<1>();
-      __syncthreads();
+      if constexpr (TMA) {
+        if (ep_armed) {
+          mbar_wait(&bars[1], ph_ep);
+          ph_ep ^= 1;
+        }
+      } else {
+        cp_async_wait<1>();
+        __syncthreads();
+      }
     }
     const int ka = f / a.n1, kb = (f + 1) / a.n1;
     const bool nba = a.tkind == 1 && (a.tdir < 0 ? ka >= 1 : ka + 1 < a.nt);
@@ -496,14 +562,21 @@ struct ColCPlan {
 // Column pass, modes as k_col (fdg_passes.cuh).  Interleaved exchange layout
 // (rows of G2 sub-lanes; split-interleaved when HOMO), sub-lanes of lane g
 // serve columns (2g, 2g+1) of the tile.
+// Tensor maps of the staged operands (FDG_TMA_COLS == 2): x (p) and acc (u)
+// viewed as [O n rows][C] doubles, box [min(n, 256) rows][W columns].
+struct ColMaps {
+  CUtensorMap x, acc;
+};
+
 template <int L, int MODE, bool PF, bool SR>
-__global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(ColArgs a) {
+__global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL)
+    k_colc(ColArgs a, const __grid_constant__ ColMaps maps) {
   using Cf = CCfg<L>;
   static_assert(Cf::OK, "split pass configuration");
   constexpr int M = Cf::M, R = Cf::R, T = Cf::T, G = Cf::G, G2 = Cf::G2, HR = Cf::HR;
   using CP = ColCPlan<L, MODE, PF, SR>;
   constexpr int LY = CP::LY, W = CP::W, P = CP::P;
-  extern __shared__ double2 smem_raw[];
+  extern __shared__ __align__(128) double2 smem_raw[];
   __shared__ double scratch[32];
   CSmem<L, SR> S(smem_raw, a.twh, a.twist, a.sym, a.sym_re);
   pdl_trigger();
@@ -521,7 +594,48 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
     const int ot = tl / ncb;
     stage_cols<W, P>(dst, src + (size_t)ot * n * C + (size_t)(tl - ot * ncb) * W, n, C);
   };
-  if constexpr (PF) {
+  // TMA staging (FDG_TMA_COLS): warp 0 issues one bulk copy per W-double row
+  // segment of the tile's operands into buffer `bi`, completion on bars[bi]
+  constexpr bool TMA = PF && FDG_TMA_COLS && P == W;
+  constexpr bool TMAP = TMA && FDG_TMA_COLS == 2;  // tensor-map boxes
+  __shared__ alignas(8) unsigned long long bars[2];
+  unsigned phb = 0;  // phase parity per buffer (bits)
+  auto stage_tma = [&](int bi, int tl) {
+    const int ot = tl / ncb;
+    const size_t off = (size_t)ot * n * C + (size_t)(tl - ot * ncb) * W;
+    const int lane = threadIdx.x & 31;
+    constexpr unsigned RB = W * sizeof(double);
+    const unsigned nops = MODE == 2 ? 2 : 1;
+    fence_proxy_async();
+    if (lane == 0) mbar_expect_tx(&bars[bi], nops * RB * (unsigned)n);
+    __syncwarp();
+    double* d0 = S.stage + bi * TILE;
+    double* d1 = S.stage + (2 + bi) * TILE;
+    if constexpr (TMAP) {  // lane 0: one box per 256 rows and operand
+      if (lane == 0) {
+        const int bh = n < 256 ? n : 256;
+        const int x = (tl - ot * ncb) * W, y0 = ot * n;
+        for (int r0 = 0; r0 < n; r0 += bh) {
+          tma_load_2d(d0 + r0 * P, &maps.x, x, y0 + r0, &bars[bi]);
+          if constexpr (MODE == 2) tma_load_2d(d1 + r0 * P, &maps.acc, x, y0 + r0, &bars[bi]);
+        }
+      }
+    } else {
+      for (int pos = lane; pos < n; pos += 32) {
+        bulk_g2s(d0 + pos * P, a.x + off + (size_t)pos * C, RB, &bars[bi]);
+        if constexpr (MODE == 2) bulk_g2s(d1 + pos * P, a.acc + off + (size_t)pos * C, RB, &bars[bi]);
+      }
+    }
+  };
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      mbar_init_fence();
+    }
+    __syncthreads();
+    if (threadIdx.x < 32 && blockIdx.x < ntiles) stage_tma(0, blockIdx.x);
+  } else if constexpr (PF) {
     if (blockIdx.x < ntiles) {
       stage_tile(S.stage, a.x, blockIdx.x);
       if constexpr (MODE == 2) stage_tile(S.stage + 2 * TILE, a.acc, blockIdx.x);
@@ -542,8 +656,14 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
     const double* st_u = S.stage + (2 + buf) * TILE;  // MODE 2
     double2 v[R];
     if constexpr (PF) {
-      cp_async_wait<0>();
-      __syncthreads();
+      if constexpr (TMA) {
+        mbar_wait(&bars[buf], (phb >> buf) & 1);
+        phb ^= 1u << buf;
+        __syncthreads();  // the other buffer's previous tile is done: it may be refilled
+      } else {
+        cp_async_wait<0>();
+        __syncthreads();
+      }
 #pragma unroll
       for (int m = 0; m < R; ++m) v[m] = *reinterpret_cast<const double2*>(st_in + (t + m * T) * P + 2 * g);
       if constexpr (MODE == 2 && FDG_K2_EREG) {
@@ -557,11 +677,15 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL) k_colc(Co
         }
       }
       if constexpr (MODE != 2) __syncthreads();  // single input buffer
-      if (nxt < ntiles) {
-        stage_tile(S.stage + (buf ^ DB) * TILE, a.x, nxt);
-        if constexpr (MODE == 2) stage_tile(S.stage + (2 + (buf ^ 1)) * TILE, a.acc, nxt);
+      if constexpr (TMA) {
+        if (nxt < ntiles && threadIdx.x < 32) stage_tma(buf ^ DB, nxt);
+      } else {
+        if (nxt < ntiles) {
+          stage_tile(S.stage + (buf ^ DB) * TILE, a.x, nxt);
+          if constexpr (MODE == 2) stage_tile(S.stage + (2 + (buf ^ 1)) * TILE, a.acc, nxt);
+        }
+        cp_async_commit();
       }
-      cp_async_commit();
     } else {
 #pragma unroll
       for (int m = 0; m < R; ++m) {

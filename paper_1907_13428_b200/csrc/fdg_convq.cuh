@@ -185,18 +185,44 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
 #pragma unroll
     for (int i = 0; i < (XPF ? HR : 1); ++i) xpre[i] = make_double2(a.xs[rx + own(i)], a.xs[rx + n + own(i)]);
   };
-  if (blockIdx.x < ntiles) {
-    stage_rows(st_in, in0 + (size_t)blockIdx.x * 2 * G * n, TILE);
-    if (MODE == 2 && !first) stage_rows(st_in2, in1 + (size_t)blockIdx.x * 2 * G * n, TILE);
-    if (upd_x) load_x(blockIdx.x);
+  // TMA staging (FDG_TMA_ROWS): barrier 0 = FFT input, 1 = epilogue operands
+  constexpr bool TMA = FDG_TMA_ROWS;
+  __shared__ alignas(8) unsigned long long bars[2];
+  constexpr unsigned TB = sizeof(double) * TILE;
+  unsigned ph_in = 0, ph_ep = 0;
+  auto stage_in = [&](int tl) {  // elected thread
+    fence_proxy_async();
+    mbar_expect_tx(&bars[0], (MODE == 2 && !first) ? 2 * TB : TB);
+    bulk_g2s(st_in, in0 + (size_t)tl * 2 * G * n, TB, &bars[0]);
+    if (MODE == 2 && !first) bulk_g2s(st_in2, in1 + (size_t)tl * 2 * G * n, TB, &bars[0]);
+  };
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      mbar_init_fence();
+      if (blockIdx.x < ntiles) stage_in(blockIdx.x);
+    }
+    if (upd_x && blockIdx.x < ntiles) load_x(blockIdx.x);
+  } else {
+    if (blockIdx.x < ntiles) {
+      stage_rows(st_in, in0 + (size_t)blockIdx.x * 2 * G * n, TILE);
+      if (MODE == 2 && !first) stage_rows(st_in2, in1 + (size_t)blockIdx.x * 2 * G * n, TILE);
+      if (upd_x) load_x(blockIdx.x);
+    }
+    cp_async_commit();
   }
-  cp_async_commit();
-  __syncthreads();  // tables
+  __syncthreads();  // tables (and the barriers' initialization)
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int f0 = tile * 2 * G;
     const size_t ra = (size_t)(f0 + 2 * g) * n;
     double2 v[16];
-    cp_async_wait<0>();
+    if constexpr (TMA) {
+      mbar_wait(&bars[0], ph_in);
+      ph_in ^= 1;
+    } else {
+      cp_async_wait<0>();
+    }
     __syncthreads();
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
@@ -232,28 +258,58 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
     __syncthreads();  // st_in and the epilogue staging are free
     const int k = f0 / a.n1;
     const bool tile_nb = a.tkind == 1 && (a.tdir < 0 ? k >= 1 : k + 1 < a.nt);
-    if (tile_nb) {
-      stage_rows(st_nb, in0 + (size_t)f0 * n + noff, TILE);
-      if (MODE == 2 && !first) stage_rows(st_nb2, in1 + (size_t)f0 * n + noff, TILE);
-    }
-    if constexpr (MODE == 1) {
-      stage_rows(st_vp, a.vp + (size_t)f0 * n, TILE);
-      if (a.r) stage_rows(st_r, (a.r_in ? a.r_in : a.r) + (size_t)f0 * n, TILE);
-    }
-    cp_async_commit();  // group E
     const int nxt = tile + gridDim.x;
-    if (nxt < ntiles) {
-      stage_rows(st_in, in0 + (size_t)nxt * 2 * G * n, TILE);
-      if (MODE == 2 && !first) stage_rows(st_in2, in1 + (size_t)nxt * 2 * G * n, TILE);
+    bool ep_armed = false;
+    if constexpr (TMA) {
+      unsigned eb = 0;
+      if (tile_nb) eb += (MODE == 2 && !first) ? 2 * TB : TB;
+      if constexpr (MODE == 1) eb += a.r ? 2 * TB : TB;
+      ep_armed = eb != 0;
+      if (threadIdx.x == 0) {
+        fence_proxy_async();
+        if (ep_armed) {
+          mbar_expect_tx(&bars[1], eb);
+          if (tile_nb) {
+            bulk_g2s(st_nb, in0 + (size_t)f0 * n + noff, TB, &bars[1]);
+            if (MODE == 2 && !first) bulk_g2s(st_nb2, in1 + (size_t)f0 * n + noff, TB, &bars[1]);
+          }
+          if constexpr (MODE == 1) {
+            bulk_g2s(st_vp, a.vp + (size_t)f0 * n, TB, &bars[1]);
+            if (a.r) bulk_g2s(st_r, (a.r_in ? a.r_in : a.r) + (size_t)f0 * n, TB, &bars[1]);
+          }
+        }
+        if (nxt < ntiles) stage_in(nxt);
+      }
+    } else {
+      if (tile_nb) {
+        stage_rows(st_nb, in0 + (size_t)f0 * n + noff, TILE);
+        if (MODE == 2 && !first) stage_rows(st_nb2, in1 + (size_t)f0 * n + noff, TILE);
+      }
+      if constexpr (MODE == 1) {
+        stage_rows(st_vp, a.vp + (size_t)f0 * n, TILE);
+        if (a.r) stage_rows(st_r, (a.r_in ? a.r_in : a.r) + (size_t)f0 * n, TILE);
+      }
+      cp_async_commit();  // group E
+      if (nxt < ntiles) {
+        stage_rows(st_in, in0 + (size_t)nxt * 2 * G * n, TILE);
+        if (MODE == 2 && !first) stage_rows(st_in2, in1 + (size_t)nxt * 2 * G * n, TILE);
+      }
+      cp_async_commit();  // group I
     }
-    cp_async_commit();  // group I
     conv_q<L, 1, GQ>(v, ex, t, gs, c, tw, a.twq, sym);
     // combine across the lane's Q sub-lanes
     __syncwarp();
     double2* sm = ex.next();
 #pragma unroll
     for (int m = 0; m < 16; ++m) sm[slot<1, 256, GQ>(t + 16 * m, gs)] = v[m];
-    cp_async_wait<1>();
+    if constexpr (TMA) {
+      if (ep_armed) {
+        mbar_wait(&bars[1], ph_ep);
+        ph_ep ^= 1;
+      }
+    } else {
+      cp_async_wait<1>();
+    }
     __syncthreads();
     double2 y[HR];
 #pragma unroll

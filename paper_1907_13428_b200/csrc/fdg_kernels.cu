@@ -10,6 +10,8 @@
 // Data layout in HBM: x[(k*n1 + i)*n2 + j], fp64, time outermost, x2
 // contiguous (problem.hpp:29-39).  No packing/zero-fill buffers: zero padding
 // and truncation of the circulant embedding happen in registers.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -835,6 +837,25 @@ cudaError_t launch_bs_post_rows(cudaStream_t st, LaunchCounter* lc, const double
   count(lc);
   k_bs_post_rows<<<ew_grid((size_t)((F + 1) / 2) * n2), EW_THREADS, 0, st>>>(v, z, F, n2, c2, scale);
   return cudaGetLastError();
+}
+
+bool encode_col_map(CUtensorMap* map, const double* base, long rows, int C, int W, int brows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) return false;
+  const cuuint64_t gdim[2] = {(cuuint64_t)C, (cuuint64_t)rows};
+  const cuuint64_t gstride[1] = {(cuuint64_t)C * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)W, (cuuint32_t)brows};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), gdim, gstride, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 size_t max_partials_needed(int nt, int n1, int n2) {

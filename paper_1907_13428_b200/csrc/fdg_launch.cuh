@@ -142,6 +142,10 @@ cudaError_t run_rowc_s(cudaStream_t st, const RowArgs& a) {
                     a);
 }
 
+// 2-D tensor map over a [rows][C] double array with a box of [brows][W]
+// (fdg_kernels.cu; driver entry point through the runtime).
+bool encode_col_map(CUtensorMap* map, const double* base, long rows, int C, int W, int brows);
+
 template <int L, int MODE, bool PF, bool SR>
 cudaError_t run_colc_s(cudaStream_t st, const ColArgs& a) {
   using Cf = CCfg<L>;
@@ -150,7 +154,14 @@ cudaError_t run_colc_s(cudaStream_t st, const ColArgs& a) {
   cudaError_t e = prep<k_colc<L, MODE, PF, SR>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
   const long tiles = (long)a.O * ((a.C + 2 * Cf::G - 1) / (2 * Cf::G));
-  return pdl_launch(PDL_KCOL, k_colc<L, MODE, PF, SR>, clamp_grid(tiles, cap), Cf::THREADS, SM, st, a);
+  ColMaps maps{};
+  if constexpr (PF && FDG_TMA_COLS == 2) {
+    constexpr int W = ColCPlan<L, MODE, PF, SR>::W;
+    const int bh = a.n < 256 ? a.n : 256;
+    if (!encode_col_map(&maps.x, a.x, (long)a.O * a.n, a.C, W, bh)) return cudaErrorInvalidValue;
+    if (MODE == 2 && !encode_col_map(&maps.acc, a.acc, (long)a.O * a.n, a.C, W, bh)) return cudaErrorInvalidValue;
+  }
+  return pdl_launch(PDL_KCOL, k_colc<L, MODE, PF, SR>, clamp_grid(tiles, cap), Cf::THREADS, SM, st, a, maps);
 }
 
 constexpr size_t kMaxSmem = 227 * 1024;

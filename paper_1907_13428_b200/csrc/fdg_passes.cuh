@@ -19,6 +19,7 @@
 // the truncation to n taken from registers (no packed workspace in HBM).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "fdg_fft.cuh"
@@ -115,6 +116,69 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
+// Bulk-copy (TMA) staging with an mbarrier per staged group: one elected
+// thread arms the barrier with the byte count and issues
+// cp.async.bulk global -> shared copies; every consumer waits on the
+// barrier's phase parity.  Replaces per-thread cp.async (LDGSTS) staging:
+// no LSU instructions or registers per staged 16 bytes.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @!P1 bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// generic-proxy accesses of the CTA before -> async-proxy (bulk copy) writes after
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// 2-D tensor-map TMA load of one box (x = column, y = row) into dst, on bar.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// One thread: a contiguous tile (bytes, multiple of 16) into dst, on bar.
+__device__ __forceinline__ void bulk_tile(double* dst, const double* src, unsigned bytes, unsigned long long* bar) {
+  fence_proxy_async();
+  mbar_expect_tx(bar, bytes);
+  bulk_g2s(dst, src, bytes, bar);
+}
+// One full warp: an n-row x W-double column tile (row stride C) into dst
+// [pos][W], one bulk copy per row segment (W * 8 bytes, a multiple of 16).
+template <int W>
+__device__ __forceinline__ void bulk_cols(double* dst, const double* src, int n, int C, unsigned long long* bar) {
+  const int lane = threadIdx.x & 31;
+  fence_proxy_async();
+  if (lane == 0) mbar_expect_tx(bar, (unsigned)(n * W * sizeof(double)));
+  __syncwarp();
+  for (int pos = lane; pos < n; pos += 32) bulk_g2s(dst + pos * W, src + (size_t)pos * C, W * sizeof(double), bar);
+}
+#ifndef FDG_TMA_P
+#define FDG_TMA_P 1  // preconditioner row passes: one bulk copy (TMA) per tile
+#endif
+#ifndef FDG_TMA_PCOL
+#define FDG_TMA_PCOL 0  // column / t passes: one bulk copy per row segment (measured slow for the S-mid pass)
+#endif
+
 // CTA-cooperative contiguous copy of `nd` doubles (nd even, 16-byte aligned).
 __device__ __forceinline__ void stage_rows(double* dst, const double* src, int nd) {
   for (int i = 2 * threadIdx.x; i < nd; i += 2 * blockDim.x) cp_async16(dst + i, src + i);
@@ -571,7 +635,16 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
   double* st_in = S.stage;
   const int g = threadIdx.x / T, t = threadIdx.x % T;  // lane-major: coalesced rows
   const int ntiles = (F + 2 * G - 1) / (2 * G);
-  if constexpr (PF) {
+  constexpr bool TMA = PF && FDG_TMA_P;
+  __shared__ alignas(8) unsigned long long bar;
+  unsigned ph = 0;
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      mbar_init_fence();
+      if (blockIdx.x < ntiles) bulk_tile(st_in, in + (size_t)blockIdx.x * TILE, 8u * TILE, &bar);
+    }
+  } else if constexpr (PF) {
     if (blockIdx.x < ntiles) stage_rows(st_in, in + (size_t)blockIdx.x * TILE, TILE);
     cp_async_commit();
   }
@@ -583,8 +656,13 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
     const size_t ia = (size_t)f * N, ib = ia + N;
     double2 v[R];
     if constexpr (PF) {
-      cp_async_wait<0>();
-      __syncthreads();
+      if constexpr (TMA) {
+        mbar_wait(&bar, ph);
+        ph ^= 1;
+      } else {
+        cp_async_wait<0>();
+        __syncthreads();
+      }
 #pragma unroll
       for (int m = 0; m < R; ++m) {
         const int pos = t + m * T;
@@ -592,8 +670,12 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
       }
       __syncthreads();
       const int nxt = tile + gridDim.x;
-      if (nxt < ntiles) stage_rows(st_in, in + (size_t)nxt * TILE, TILE);
-      cp_async_commit();
+      if constexpr (TMA) {
+        if (threadIdx.x == 0 && nxt < ntiles) bulk_tile(st_in, in + (size_t)nxt * TILE, 8u * TILE, &bar);
+      } else {
+        if (nxt < ntiles) stage_rows(st_in, in + (size_t)nxt * TILE, TILE);
+        cp_async_commit();
+      }
     } else {
 #pragma unroll
       for (int m = 0; m < R; ++m) {
@@ -640,11 +722,22 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
   const int g = threadIdx.x % G, t = threadIdx.x / G;
   const int ncb = (C + W - 1) / W;
   const int ntiles = ncb * O;
-  if constexpr (PF) {
-    if (blockIdx.x < ntiles) {
-      const int o = blockIdx.x / ncb;
-      stage_cols<W>(st_in, data + (size_t)o * N * C + (size_t)(blockIdx.x - o * ncb) * W, N, C);
+  constexpr bool TMA = PF && FDG_TMA_PCOL;
+  __shared__ alignas(8) unsigned long long bar;
+  unsigned ph = 0;
+  auto src_of = [&](int tl) {
+    const int ot = tl / ncb;
+    return data + (size_t)ot * N * C + (size_t)(tl - ot * ncb) * W;
+  };
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      mbar_init_fence();
     }
+    __syncthreads();
+    if (threadIdx.x < 32 && blockIdx.x < ntiles) bulk_cols<W>(st_in, src_of(blockIdx.x), N, C, &bar);
+  } else if constexpr (PF) {
+    if (blockIdx.x < ntiles) stage_cols<W>(st_in, src_of(blockIdx.x), N, C);
     cp_async_commit();
   }
   __syncthreads();
@@ -655,17 +748,23 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
     double* base = data + (size_t)o * N * C + c;
     double2 v[R];
     if constexpr (PF) {
-      cp_async_wait<0>();
-      __syncthreads();
+      if constexpr (TMA) {
+        mbar_wait(&bar, ph);
+        ph ^= 1;
+      } else {
+        cp_async_wait<0>();
+        __syncthreads();
+      }
 #pragma unroll
       for (int m = 0; m < R; ++m) v[m] = *reinterpret_cast<const double2*>(st_in + (t + m * T) * W + 2 * g);
       __syncthreads();
       const int nxt = tile + gridDim.x;
-      if (nxt < ntiles) {
-        const int on = nxt / ncb;
-        stage_cols<W>(st_in, data + (size_t)on * N * C + (size_t)(nxt - on * ncb) * W, N, C);
+      if constexpr (TMA) {
+        if (threadIdx.x < 32 && nxt < ntiles) bulk_cols<W>(st_in, src_of(nxt), N, C, &bar);
+      } else {
+        if (nxt < ntiles) stage_cols<W>(st_in, src_of(nxt), N, C);
+        cp_async_commit();
       }
-      cp_async_commit();
     } else {
 #pragma unroll
       for (int m = 0; m < R; ++m)
@@ -698,7 +797,17 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(doub
   const int g = threadIdx.x % G, t = threadIdx.x / G;
   const int C = pt.n1 * pt.n2;
   const int ntiles = (C + W - 1) / W;
-  if constexpr (PF) {
+  constexpr bool TMA = PF && FDG_TMA_PCOL;
+  __shared__ alignas(8) unsigned long long bar;
+  unsigned ph = 0;
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      mbar_init_fence();
+    }
+    __syncthreads();
+    if (threadIdx.x < 32 && blockIdx.x < ntiles) bulk_cols<W>(st_in, data + (size_t)blockIdx.x * W, N, C, &bar);
+  } else if constexpr (PF) {
     if (blockIdx.x < ntiles) stage_cols<W>(st_in, data + (size_t)blockIdx.x * W, N, C);
     cp_async_commit();
   }
@@ -708,14 +817,23 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(doub
     const bool vc = PF || c < C;
     double2 v[R];
     if constexpr (PF) {
-      cp_async_wait<0>();
-      __syncthreads();
+      if constexpr (TMA) {
+        mbar_wait(&bar, ph);
+        ph ^= 1;
+      } else {
+        cp_async_wait<0>();
+        __syncthreads();
+      }
 #pragma unroll
       for (int m = 0; m < R; ++m) v[m] = *reinterpret_cast<const double2*>(st_in + (t + m * T) * W + 2 * g);
       __syncthreads();
       const int nxt = tile + gridDim.x;
-      if (nxt < ntiles) stage_cols<W>(st_in, data + (size_t)nxt * W, N, C);
-      cp_async_commit();
+      if constexpr (TMA) {
+        if (threadIdx.x < 32 && nxt < ntiles) bulk_cols<W>(st_in, data + (size_t)nxt * W, N, C, &bar);
+      } else {
+        if (nxt < ntiles) stage_cols<W>(st_in, data + (size_t)nxt * W, N, C);
+        cp_async_commit();
+      }
     } else {
 #pragma unroll
       for (int m = 0; m < R; ++m)

@@ -48,6 +48,9 @@ constexpr int PH = 16;       // mirror-pair rounds: k = t + 33 m < 512 for m < 1
 #ifndef FDG_PFA_GCOL
 #define FDG_PFA_GCOL 7
 #endif
+#ifndef FDG_PFA_TMA
+#define FDG_PFA_TMA 1  // bulk-copy (TMA) staging of the row passes
+#endif
 template <int G>
 struct PCfg {
   static constexpr int THREADS = (PA * G + 31) / 32 * 32;
@@ -259,28 +262,51 @@ __global__ void __launch_bounds__(PCfg<PG>::THREADS, PCfg<PG>::MINB)
   const int gl = act ? g : 0;  // idle threads shadow lane 0 (stores off)
   double2* E = Ex + gl * PN;
   const long ntiles = (F + 2 * PG - 1) / (2 * PG);
+  // staging: one bulk copy (TMA) of the tile's rows per tile, completion on
+  // an mbarrier (F even: every tile is a multiple of 16 bytes), else
+  // per-thread cp.async
+  __shared__ alignas(8) unsigned long long bar;
+  const bool tma = FDG_PFA_TMA && (F & 1) == 0;
+  unsigned ph = 0;
   auto stage = [&](long tile) {
     const long r0 = tile * 2 * PG;
     const long nr = F - r0 < 2 * PG ? F - r0 : 2 * PG;
     const int nd = (int)(nr * PN);
     const double* src = in + r0 * PN;
-    for (int i = 2 * tid; i + 1 < nd; i += 2 * PTHREADS) cp_async16(S + i, src + i);
-    if ((nd & 1) && tid == 0) S[nd - 1] = src[nd - 1];
+    if (tma) {
+      if (tid == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(&bar, 8u * nd);
+        bulk_g2s(S, src, 8u * nd, &bar);
+      }
+    } else {
+      for (int i = 2 * tid; i + 1 < nd; i += 2 * PTHREADS) cp_async16(S + i, src + i);
+      if ((nd & 1) && tid == 0) S[nd - 1] = src[nd - 1];
+      cp_async_commit();
+    }
   };
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
   if (blockIdx.x < ntiles) stage(blockIdx.x);
-  cp_async_commit();
   for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const long f = tile * 2 * PG + 2 * g;  // the lane's first row
     const bool va = act && f < F, vb = act && f + 1 < F;
-    cp_async_wait<0>();
-    __syncthreads();
+    if (tma) {
+      mbar_wait(&bar, ph);
+      ph ^= 1;
+    } else {
+      cp_async_wait<0>();
+      __syncthreads();
+    }
     const int t = opaque(t0);
     const double* ra = S + 2 * gl * PN;
     pfa_dft(
         E, t, act, [&](int n) { return make_double2(va ? ra[n] : 0.0, vb ? ra[PN + n] : 0.0); },
         [&] {  // S free: the next tile's rows stream in during the rest of the transform
           if (tile + (long)gridDim.x < ntiles) stage(tile + gridDim.x);
-          cp_async_commit();
         });
     if (va) {
       double* oa = out + f * PN;
@@ -366,8 +392,12 @@ __global__ void __launch_bounds__(PCfg<PG>::THREADS, PCfg<PG>::MINB)
       const int ca = c0 + 2 * gl;
       const double l2a = __ldg(&lam2[ca]);
       const double l2b = vb ? __ldg(&lam2[ca + 1]) : l2a;
-      auto divide = [&](double2 z, int k) {
-        const double l1 = __ldg(&lam1[k]);
+      // lambda_1 of the thread's 16 pair positions, loaded as one batch (the
+      // spectrum is even, lam1[1023 - k] = lam1[k], checked at creation)
+      double l1v[PH];
+#pragma unroll
+      for (int m = 0; m < PH; ++m) l1v[m] = __ldg(&lam1[t + PA * m]);
+      auto divide = [&](double2 z, int k, double l1) {
         const double da = l1 + l2a, db = l1 + l2b;
         const double inv = frcp(da * db);  // one reciprocal for both columns
         if (act) Sh[k] = make_double2(z.x * (db * inv), vb ? z.y * (da * inv) : 0.0);
@@ -378,8 +408,8 @@ __global__ void __launch_bounds__(PCfg<PG>::THREADS, PCfg<PG>::MINB)
         const int k = t + PA * m;
         if (k < PN / 2 + 1) {  // mirror pair (k, 1023 - k)
           const double2 zk = E[ms.k()], zm = E[ms.km()];
-          divide(hartley_split(zk, zm), k);
-          if (k) divide(hartley_split(zm, zk), PN - k);
+          divide(hartley_split(zk, zm), k, l1v[m]);
+          if (k) divide(hartley_split(zm, zk), PN - k, l1v[m]);
         }
       }
     }
