@@ -310,8 +310,13 @@ cudaError_t run_hcol_v(cudaStream_t st, double* data, int O, int C, const double
   int cap = 0;
   cudaError_t e = prep<k_hartley_col<N, PF>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
+  CUtensorMap map{};
+  if constexpr (PF && FDG_TMA_PCOL == 2) {
+    if (!encode_col_map(&map, data, (long)O * N, C, 2 * Cf::G, N < 256 ? N : 256)) return cudaErrorInvalidValue;
+  }
   const long tiles = (long)O * ((C + 2 * Cf::G - 1) / (2 * Cf::G));
-  return pdl_launch(PDL_PCOL | (PF ? 0 : PDL_L1), k_hartley_col<N, PF>, clamp_grid(tiles, cap), Cf::THREADS, SM, st, data, O, C, tw, guard);
+  return pdl_launch(PDL_PCOL | (PF ? 0 : PDL_L1), k_hartley_col<N, PF>, clamp_grid(tiles, cap), Cf::THREADS, SM, st, data, O, C, tw, guard,
+                    map);
 }
 
 template <int N>
@@ -329,9 +334,13 @@ cudaError_t run_tf_v(cudaStream_t st, double* data, const PcTables& pt, const in
   int cap = 0;
   cudaError_t e = prep<k_t_filter<N, PF>>(SM, Cf::THREADS, cap);
   if (e != cudaSuccess) return e;
+  CUtensorMap map{};
+  if constexpr (PF && FDG_TMA_PCOL == 2) {
+    if (!encode_col_map(&map, data, N, pt.n1 * pt.n2, 2 * Cf::G, N < 256 ? N : 256)) return cudaErrorInvalidValue;
+  }
   const long C = (long)pt.n1 * pt.n2;
   return pdl_launch(PDL_TF | (PF ? 0 : PDL_L1), k_t_filter<N, PF>, clamp_grid((C + 2 * Cf::G - 1) / (2 * Cf::G), cap), Cf::THREADS, SM, st, data,
-                    pt, guard);
+                    pt, guard, map);
 }
 
 template <int N>

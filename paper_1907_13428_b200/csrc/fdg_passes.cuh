@@ -176,8 +176,19 @@ __device__ __forceinline__ void bulk_cols(double* dst, const double* src, int n,
 #define FDG_TMA_P 1  // preconditioner row passes: one bulk copy (TMA) per tile
 #endif
 #ifndef FDG_TMA_PCOL
-#define FDG_TMA_PCOL 0  // column / t passes: one bulk copy per row segment (measured slow for the S-mid pass)
+#define FDG_TMA_PCOL 2  // column / t passes: 2 = 2-D tensor-map boxes, 1 = one bulk copy per row segment
+                        // (measured slow), 0 = per-thread cp.async
 #endif
+// One thread: an n-row x W-double column tile at (column x, row y) of a 2-D
+// tensor map, in boxes of min(n, 256) rows, into dst [pos][W], on bar.
+template <int W>
+__device__ __forceinline__ void tma_cols(double* dst, const CUtensorMap* map, int x, int y, int n,
+                                         unsigned long long* bar) {
+  fence_proxy_async();
+  mbar_expect_tx(bar, (unsigned)(n * W * sizeof(double)));
+  const int bh = n < 256 ? n : 256;
+  for (int r0 = 0; r0 < n; r0 += bh) tma_load_2d(dst + r0 * W, map, x, y + r0, bar);
+}
 
 // CTA-cooperative contiguous copy of `nd` doubles (nd even, 16-byte aligned).
 __device__ __forceinline__ void stage_rows(double* dst, const double* src, int nd) {
@@ -278,7 +289,7 @@ __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_row(RowArgs a
   using RP = RowPlan<L, MODE, PF>;
   constexpr int R = C::R, T = C::T, G = C::G, H = (R + 1) / 2;
   constexpr int TILE = RP::TILE;
-  extern __shared__ double2 smem_raw[];
+  extern __shared__ __align__(128) double2 smem_raw[];
   __shared__ double scratch[32];
   Smem<L, RP::DB> S(smem_raw, a.tw, 0);
   pdl_trigger();
@@ -497,7 +508,7 @@ __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_col(ColArgs a
   using Cf = Cfg<L>;
   constexpr int R = Cf::R, T = Cf::T, G = Cf::G, H = (R + 1) / 2;
   constexpr int W = 2 * G;  // columns per tile
-  extern __shared__ double2 smem_raw[];
+  extern __shared__ __align__(128) double2 smem_raw[];
   __shared__ double scratch[32];
   Smem<L, Cf::DB> S(smem_raw, a.tw, 0);
   pdl_trigger();
@@ -626,7 +637,7 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
   using Cf = Cfg<N>;
   constexpr int R = Cf::R, T = Cf::T, G = Cf::G;
   constexpr int TILE = HPlan<N, PF>::TILE;
-  extern __shared__ double2 smem_raw[];
+  extern __shared__ __align__(128) double2 smem_raw[];
   __shared__ double scratch[32];
   Smem<N, Cf::DB> S(smem_raw, tw, 0);
   pdl_trigger();
@@ -709,11 +720,12 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
 
 template <int N, bool PF>
 __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
-    k_hartley_col(double* data, int O, int C, const double2* tw, const int* guard) {
+    k_hartley_col(double* data, int O, int C, const double2* tw, const int* guard,
+                  const __grid_constant__ CUtensorMap map) {
   using Cf = Cfg<N>;
   constexpr int R = Cf::R, T = Cf::T, G = Cf::G;
   constexpr int W = 2 * G;
-  extern __shared__ double2 smem_raw[];
+  extern __shared__ __align__(128) double2 smem_raw[];
   Smem<N, Cf::DB> S(smem_raw, tw, 0);
   pdl_trigger();
   pdl_wait();
@@ -729,13 +741,23 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
     const int ot = tl / ncb;
     return data + (size_t)ot * N * C + (size_t)(tl - ot * ncb) * W;
   };
+  auto stage_tma = [&](int tl) {  // one box per 256 rows (2-D map), or one bulk copy per row (warp 0)
+    if constexpr (FDG_TMA_PCOL == 2) {
+      if (threadIdx.x == 0) {
+        const int ot = tl / ncb;
+        tma_cols<W>(st_in, &map, (tl - ot * ncb) * W, ot * N, N, &bar);
+      }
+    } else if (threadIdx.x < 32) {
+      bulk_cols<W>(st_in, src_of(tl), N, C, &bar);
+    }
+  };
   if constexpr (TMA) {
     if (threadIdx.x == 0) {
       mbar_init(&bar, 1);
       mbar_init_fence();
     }
     __syncthreads();
-    if (threadIdx.x < 32 && blockIdx.x < ntiles) bulk_cols<W>(st_in, src_of(blockIdx.x), N, C, &bar);
+    if (blockIdx.x < ntiles) stage_tma(blockIdx.x);
   } else if constexpr (PF) {
     if (blockIdx.x < ntiles) stage_cols<W>(st_in, src_of(blockIdx.x), N, C);
     cp_async_commit();
@@ -760,7 +782,7 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
       __syncthreads();
       const int nxt = tile + gridDim.x;
       if constexpr (TMA) {
-        if (threadIdx.x < 32 && nxt < ntiles) bulk_cols<W>(st_in, src_of(nxt), N, C, &bar);
+        if (nxt < ntiles) stage_tma(nxt);
       } else {
         if (nxt < ntiles) stage_cols<W>(st_in, src_of(nxt), N, C);
         cp_async_commit();
@@ -782,11 +804,12 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB)
 // in registers from the 1-D eigenvalues, circulant.cpp:28-41, 76-90) and by
 // N (circulant.cpp:62-64), Hartley along t again.
 template <int N, bool PF>
-__global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(double* data, PcTables pt, const int* guard) {
+__global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(double* data, PcTables pt, const int* guard,
+                                                                              const __grid_constant__ CUtensorMap map) {
   using Cf = Cfg<N>;
   constexpr int R = Cf::R, T = Cf::T, G = Cf::G;
   constexpr int W = 2 * G;
-  extern __shared__ double2 smem_raw[];
+  extern __shared__ __align__(128) double2 smem_raw[];
   Smem<N, Cf::DB> S(smem_raw, pt.tw_t, N);
   load_table(S.tab, pt.lam_t, N);
   pdl_trigger();
@@ -800,13 +823,20 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(doub
   constexpr bool TMA = PF && FDG_TMA_PCOL;
   __shared__ alignas(8) unsigned long long bar;
   unsigned ph = 0;
+  auto stage_tma = [&](int tl) {
+    if constexpr (FDG_TMA_PCOL == 2) {
+      if (threadIdx.x == 0) tma_cols<W>(st_in, &map, tl * W, 0, N, &bar);
+    } else if (threadIdx.x < 32) {
+      bulk_cols<W>(st_in, data + (size_t)tl * W, N, C, &bar);
+    }
+  };
   if constexpr (TMA) {
     if (threadIdx.x == 0) {
       mbar_init(&bar, 1);
       mbar_init_fence();
     }
     __syncthreads();
-    if (threadIdx.x < 32 && blockIdx.x < ntiles) bulk_cols<W>(st_in, data + (size_t)blockIdx.x * W, N, C, &bar);
+    if (blockIdx.x < ntiles) stage_tma(blockIdx.x);
   } else if constexpr (PF) {
     if (blockIdx.x < ntiles) stage_cols<W>(st_in, data + (size_t)blockIdx.x * W, N, C);
     cp_async_commit();
@@ -829,7 +859,7 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(doub
       __syncthreads();
       const int nxt = tile + gridDim.x;
       if constexpr (TMA) {
-        if (threadIdx.x < 32 && nxt < ntiles) bulk_cols<W>(st_in, data + (size_t)nxt * W, N, C, &bar);
+        if (nxt < ntiles) stage_tma(nxt);
       } else {
         if (nxt < ntiles) stage_cols<W>(st_in, data + (size_t)nxt * W, N, C);
         cp_async_commit();
