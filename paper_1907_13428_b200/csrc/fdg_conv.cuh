@@ -57,6 +57,15 @@ namespace fdg {
 #ifndef FDG_C_COLLY
 #define FDG_C_COLLY 2
 #endif
+#ifndef FDG_C1024_COLLY
+#define FDG_C1024_COLLY FDG_C_COLLY
+#endif
+#ifndef FDG_C2048_COLLY
+#define FDG_C2048_COLLY FDG_C_COLLY
+#endif
+#ifndef FDG_K2_WOWN
+#define FDG_K2_WOWN 1  // S-mid column pass: second convolution's input from the owned registers + the partner's half
+#endif
 #ifndef FDG_TMA_ROWS
 #define FDG_TMA_ROWS 1  // staged split row passes: bulk-copy (TMA) staging with mbarriers
 #endif
@@ -67,6 +76,36 @@ namespace fdg {
 #ifndef FDG_K2_EREG
 #define FDG_K2_EREG 1  // S-mid column pass: a1 p^T p from the input registers
 #endif
+
+// Twist factors W_L^(t + T m) = W_L^t W_32^m (T = L/32 at R = 16) formed as a
+// compile-time constant multiply times one per-thread value instead of a table
+// load per element, where the table is not in shared memory (M = 1024: loads
+// through L1; measured slower where the table is staged, C2 K2 223 -> 235 us):
+// bit 0 = the odd half's pre-twist, bit 1 = the post-twist in the combine.
+#ifndef FDG_TWIST_CONST
+#define FDG_TWIST_CONST 3
+#endif
+
+// x W_32^Q (CONJ: x conj(W_32^Q)), W_32 = exp(-2 pi i / 32), compile-time Q in [0, 16).
+template <int Q, bool CONJ>
+__device__ __forceinline__ double2 mul_w32(double2 x) {
+  static_assert(Q >= 0 && Q < 16, "twist constant index");
+  constexpr double H = 0.70710678118654752440;
+  constexpr double C1 = 0.92387953251128675613, S1 = 0.38268343236508977173;  // pi/8
+  constexpr double CA = 0.98078528040323044913, SA = 0.19509032201612826785;  // pi/16
+  constexpr double CB = 0.83146961230254523708, SB = 0.55557023301960222474;  // 3 pi/16
+  constexpr double cs[16] = {1, CA, C1, CB, H, SB, S1, SA, 0, -SA, -S1, -SB, -H, -CB, -C1, -CA};
+  constexpr double sn[16] = {0, SA, S1, SB, H, CB, C1, CA, 1, CA, C1, CB, H, SB, S1, SA};
+  constexpr double c = cs[Q];
+  constexpr double s = CONJ ? -sn[Q] : sn[Q];  // x (c - i s)
+  if constexpr (Q == 0) {
+    return x;
+  } else if constexpr (Q == 8) {
+    return make_double2(s * x.y, -s * x.x);
+  } else {
+    return make_double2(fma(s, x.y, c * x.x), fma(-s, x.x, c * x.y));
+  }
+}
 
 template <int L>
 struct CCfg {
@@ -90,6 +129,9 @@ struct CCfg {
   // twist table in shared memory up to M = 512 (else read through L1, which
   // leaves room for four staged tiles at L = 2048)
   static constexpr bool TWS = M <= 512;
+  // twist by constants (needs L / T == 32)
+  static constexpr bool TWC_PRE = R == 16 && !TWS && (FDG_TWIST_CONST & 1);
+  static constexpr bool TWC_POST = R == 16 && !TWS && (FDG_TWIST_CONST & 2);
   // exchange | M-point twiddles | twist W_L^j (j < M) | symbol (L, real or
   // complex) | staging
   static constexpr size_t bytes(size_t stage_doubles, bool sr) {
@@ -206,6 +248,22 @@ __device__ __forceinline__ void pair_sync(int g = 0) {
   }
 }
 
+// v[m] *= W_32^m wt for every m (compile-time recursion over m).
+template <int Q, int R>
+__device__ __forceinline__ void twist_const(double2 (&v)[R], double2 wt) {
+  if constexpr (Q < R) {
+    v[Q] = cmul(mul_w32<Q, false>(v[Q]), wt);
+    twist_const<Q + 1>(v, wt);
+  }
+}
+// x conj(W_L^pos) for pos = t + T (I + b R/2): conj(W_32^I) (+i)^b conj(wt).
+template <int I>
+__device__ __forceinline__ double2 untwist_const(double2 x, int b, double2 wt) {
+  double2 y = mul_w32<I, true>(x);
+  if (b) y = make_double2(-y.y, y.x);
+  return cmulc(y, wt);
+}
+
 // Sub-lane b's half of the convolution, in place on v (input z[t + T m] for
 // every m; output that half's contribution at the same positions).
 #ifndef FDG_BAL_TWIST
@@ -220,8 +278,13 @@ __device__ __forceinline__ void conv_half(double2 (&v)[CCfg<L>::R], Ex& ex, int 
   constexpr int M = C::M, R = C::R, T = C::T, G2 = C::G2;
   constexpr bool CACHE = FDG_TWCACHE && TwCache<M, R>::OK;
   if (b) {
+    if constexpr (C::TWC_PRE) {
+      const double2 wt = twist[t];
+      twist_const<0>(v, wt);
+    } else {
 #pragma unroll
-    for (int m = 0; m < R; ++m) v[m] = cmul(v[m], twist[t + T * m]);
+      for (int m = 0; m < R; ++m) v[m] = cmul(v[m], twist[t + T * m]);
+    }
   }
   double2 wc[TwCache<M, R>::K];
   fft_lane_c<M, R, G2, false, LAYOUT, CACHE ? 1 : 0>(v, ex, t, gs, tw, wc);
@@ -233,6 +296,25 @@ __device__ __forceinline__ void conv_half(double2 (&v)[CCfg<L>::R], Ex& ex, int 
   if (b && !FDG_BAL_TWIST) {
 #pragma unroll
     for (int m = 0; m < R; ++m) v[m] = cmulc(v[m], twist[t + T * m]);
+  }
+}
+
+// conv_combine's read-and-add with the odd values' post-twist formed from
+// constants (compile-time recursion over the owned positions).
+template <int I, int L, int LAYOUT, class Map>
+__device__ __forceinline__ void combine_const(const double2 (&v)[CCfg<L>::R], double2 (&y)[CCfg<L>::HR],
+                                              const double2* sm, const Map& mp, double2 wt) {
+  using C = CCfg<L>;
+  constexpr int M = C::M, T = C::T, G2 = C::G2, HR = C::HR;
+  if constexpr (I < HR) {
+    const int b = mp.b;
+    const int pos = mp.t + T * (I + b * HR);
+    double2 mine = b ? v[I + HR] : v[I];
+    double2 other = sm[slot<LAYOUT, M, G2>(pos, mp.partner)];
+    if (b) mine = untwist_const<I>(mine, 1, wt);
+    else other = untwist_const<I>(other, 0, wt);
+    y[I] = cadd(mine, other);
+    combine_const<I + 1, L, LAYOUT>(v, y, sm, mp, wt);
   }
 }
 
@@ -258,17 +340,21 @@ __device__ __forceinline__ void conv_combine(const double2 (&v)[CCfg<L>::R], dou
     sm[slot<LAYOUT, M, G2>(t + T * (b ? i : i + HR), mp.gs)] = val;
   }
   pair_sync<L, LAYOUT, HM>(mp.g);
+  if constexpr (C::TWC_POST && FDG_BAL_TWIST) {
+    combine_const<0, L, LAYOUT>(v, y, sm, mp, twist[t]);
+  } else {
 #pragma unroll
-  for (int i = 0; i < HR; ++i) {
-    const int pos = t + T * (i + b * HR);
-    double2 mine = b ? v[i + HR] : v[i];
-    double2 other = sm[slot<LAYOUT, M, G2>(pos, mp.partner)];
+    for (int i = 0; i < HR; ++i) {
+      const int pos = t + T * (i + b * HR);
+      double2 mine = b ? v[i + HR] : v[i];
+      double2 other = sm[slot<LAYOUT, M, G2>(pos, mp.partner)];
 #if FDG_BAL_TWIST
-    const double2 w = twist[pos];
-    if (b) mine = cmulc(mine, w);
-    else other = cmulc(other, w);
+      const double2 w = twist[pos];
+      if (b) mine = cmulc(mine, w);
+      else other = cmulc(other, w);
 #endif
-    y[i] = cadd(mine, other);
+      y[i] = cadd(mine, other);
+    }
   }
   if constexpr (TRAIL) pair_sync<L, LAYOUT, HM>(mp.g);
 }
@@ -550,7 +636,8 @@ struct ColCPlan {
   using C = CCfg<L>;
   // exchange layout: 1 = lane-major (sub-lane-local exchanges, __syncwarp),
   // else interleaved rows (CTA-wide barriers)
-  static constexpr int LY = FDG_C_COLLY == 1 ? 1 : (C::HOMO_COL ? 2 : 0);
+  static constexpr int LY_SEL = L == 1024 ? FDG_C1024_COLLY : (L == 2048 ? FDG_C2048_COLLY : FDG_C_COLLY);
+  static constexpr int LY = LY_SEL == 1 ? 1 : (C::HOMO_COL ? 2 : 0);
   static constexpr int W = 2 * C::G;              // columns per tile
   static constexpr int P = LY == 1 ? W + 2 : W;   // staged row pitch (bank spread)
   static constexpr int TILE = PF ? C::M * P : 0;  // doubles per staged operand
@@ -735,19 +822,30 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL)
       }
       // both halves need all of w: each writes its positions into its own
       // slot column, then reads the lane's full column pair
-      pair_sync<L, LY, Cf::HOMO_COL>();  // write-after-read: combine
+      pair_sync<L, LY, Cf::HOMO_COL>(mp.g);  // write-after-read: combine
       double2* sm = S.ex.next();
 #pragma unroll
       for (int i = 0; i < HR; ++i) sm[slot<LY, M, G2>(t + T * (i + b * HR), mp.gs)] = y[i];
-      pair_sync<L, LY, Cf::HOMO_COL>();
+      pair_sync<L, LY, Cf::HOMO_COL>(mp.g);
+#if FDG_K2_WOWN
+      // the owned half of w is still in registers: only the partner's half
+      // comes back from the exchange
+#pragma unroll
+      for (int i = 0; i < HR; ++i) {
+        const double2 other = sm[slot<LY, M, G2>(t + T * (i + (1 - b) * HR), mp.partner)];
+        v[i] = b ? other : y[i];
+        v[i + HR] = b ? y[i] : other;
+      }
+#else
       const int id0 = mp.half_id(0), id1 = mp.half_id(1);
 #pragma unroll
       for (int m = 0; m < R; ++m) v[m] = sm[slot<LY, M, G2>(t + T * m, m < HR ? id0 : id1)];
+#endif
       // write-after-read across the halves: each half reads the other's
       // slots above, and the first scatter of its transform below is guarded
       // only by its own half barrier (lane_sync), so a lagging half could
       // still be reading the slots the other half overwrites
-      pair_sync<L, LY, Cf::HOMO_COL>();
+      pair_sync<L, LY, Cf::HOMO_COL>(mp.g);
       conv_half<L, LY>(v, S.ex, t, mp.gs, b, S.tw, S.twist, S.sym);
       conv_combine<L, LY, !PF>(v, y, S.ex, mp, S.twist);
 #pragma unroll

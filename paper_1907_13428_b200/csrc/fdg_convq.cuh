@@ -26,6 +26,10 @@
 
 namespace fdg {
 
+#ifndef FDG_Q_TRIV
+#define FDG_Q_TRIV 1  // trivial factors without multiplies: residue 0's twist, the W_4^c input combination
+#endif
+
 template <int L, bool ROWS>
 struct QCfg {
   static constexpr int Q = L >= 1024 ? L / 256 : 4;  // sub-lanes per lane (other L: unused)
@@ -94,8 +98,11 @@ __device__ __forceinline__ void conv_q(double2 (&v)[16], Ex& ex, int t, int gs, 
                                        const double2* twq, const double* sym) {
   constexpr int Q = L / 256;
   constexpr bool CACHE = FDG_TWCACHE != 0;
+  // residue 0 has no twist (c is uniform over a warp)
+  if (c != 0 || !FDG_Q_TRIV) {
 #pragma unroll
-  for (int m = 0; m < 16; ++m) v[m] = cmul(v[m], __ldg(&twq[(t + 16 * m) * c]));
+    for (int m = 0; m < 16; ++m) v[m] = cmul(v[m], __ldg(&twq[(t + 16 * m) * c]));
+  }
   double2 wc[TwCache<256, 16>::K];
   fft_lane_c<256, 16, GQ, false, LAYOUT, CACHE ? 1 : 0>(v, ex, t, gs, tw, wc);
 #pragma unroll
@@ -103,8 +110,10 @@ __device__ __forceinline__ void conv_q(double2 (&v)[16], Ex& ex, int t, int gs, 
   fft_lane_c<256, 16, GQ, true, LAYOUT, CACHE ? 2 : 0>(v, ex, t, gs, tw, wc);
   // W_L^{-j c} read as W_L^{L - j c}: distinct addresses from the forward
   // twist, so no 64-bit address stays live across the transforms
+  if (c != 0 || !FDG_Q_TRIV) {
 #pragma unroll
-  for (int m = 0; m < 16; ++m) v[m] = cmul(v[m], __ldg(&twq[(L - (t + 16 * m) * c) & (L - 1)]));
+    for (int m = 0; m < 16; ++m) v[m] = cmul(v[m], __ldg(&twq[(L - (t + 16 * m) * c) & (L - 1)]));
+  }
 }
 
 template <int L, int MODE, bool SR>
@@ -163,6 +172,8 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
   double2 win[NB];
 #pragma unroll
   for (int bb = 0; bb < NB; ++bb) win[bb] = wq_const<Q>(bb * c);
+  // Q = 4: z W_4^c = (rsx p, rsy q) with (p, q) = (z.x, z.y), swapped for odd c
+  const double rsx = (c & 2) ? -1.0 : 1.0, rsy = (c == 1 || c == 2) ? -1.0 : 1.0;
   double alpha = 0.0, beta = 0.0;
   if constexpr (MODE == 1) {
     if (a.r) alpha = *a.a_num / *a.a_den;
@@ -248,7 +259,17 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
             }
           }
         }
-        u = bb == 0 ? z : cadd(u, cmul(z, win[bb]));
+        if constexpr (Q == 4 && FDG_Q_TRIV) {
+          // W_4^c: a quarter-turn count, by one swap and two signed adds
+          if (bb == 0) {
+            u = z;
+          } else {
+            const double p = (c & 1) ? z.y : z.x, q = (c & 1) ? z.x : z.y;
+            u = make_double2(fma(rsx, p, u.x), fma(rsy, q, u.y));
+          }
+        } else {
+          u = bb == 0 ? z : cadd(u, cmul(z, win[bb]));
+        }
       }
       v[m] = u;
     }

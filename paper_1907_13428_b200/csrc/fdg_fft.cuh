@@ -324,6 +324,30 @@ struct TwCache {
   static constexpr int K = OK ? R : 1;  // S * Rp of the twiddled pass
 };
 
+// Last pass of a three-pass plan (S > 1 butterflies per thread, N / T = 16):
+// butterfly s of thread t sits at b = t + s T, so its twiddles factor as
+// W_N^(b r) = (W_N^t)^r W_16^(s r): the Rp - 1 per-thread values are loaded
+// once and the rest are compile-time constant multiplies (the shared-memory
+// pipe, not FP64, is the busier unit: 3 loads instead of 12 at N = 1024).
+#ifndef FDG_TW_LASTC
+#define FDG_TW_LASTC 1
+#endif
+template <int Rp, int S, bool INV, int Sx = 1, int Rx = 1>
+struct LastTwiddle {
+  template <int R>
+  __device__ __forceinline__ static void run(double2 (&v)[R], const double2 (&wt)[Rp]) {
+    if constexpr (Sx < S) {
+      if constexpr (Rx < Rp) {
+        const double2 x = mul_wq<16, (Sx * Rx) % 16, INV>(v[Sx + Rx * S]);
+        v[Sx + Rx * S] = INV ? cmulc(x, wt[Rx]) : cmul(x, wt[Rx]);
+        LastTwiddle<Rp, S, INV, Sx, Rx + 1>::run(v, wt);
+      } else {
+        LastTwiddle<Rp, S, INV, Sx + 1, 1>::run(v, wt);
+      }
+    }
+  }
+};
+
 template <int N, int R, int G, bool INV, int Ns, int LAYOUT, int OFF = 0, int CM = 0>
 struct Stockham {
   static constexpr int T = N / R;
@@ -342,6 +366,24 @@ struct Stockham {
   __device__ __forceinline__ static void run(double2 (&v)[R], Ex& ex, int t, int g, const double2* ptw,
                                              double2 (&wc)[CK]) {
     static_assert(CM == 0 || (TwCache<N, R>::OK && CK >= TwCache<N, R>::K), "twiddle cache shape");
+    constexpr bool LASTC = FDG_TW_LASTC && LAST && Ns > 1 && S > 1 && R == 16 && CM == 0 && T <= Ns;
+    if constexpr (LASTC) {
+      double2 wt[Rp];
+#pragma unroll
+      for (int r = 1; r < Rp; ++r) {
+        if ((r & (r - 1)) == 0) {
+          wt[r] = ptw[OFF + (r - 1) * Ns + t];
+        } else {
+          const int lo = r & -r;
+          wt[r] = cmul(wt[lo], wt[r - lo]);
+        }
+      }
+#pragma unroll
+      for (int r = 1; r < Rp; ++r) v[r * S] = INV ? cmulc(v[r * S], wt[r]) : cmul(v[r * S], wt[r]);
+      LastTwiddle<Rp, S, INV>::run(v, wt);
+#pragma unroll
+      for (int s = 0; s < S; ++s) Dft<Rp, INV>::run(v, s, S);
+    } else {
 #pragma unroll
     for (int s = 0; s < S; ++s) {
       const int b = t + s * T;  // butterfly index in [0, N/Rp)
@@ -373,6 +415,7 @@ struct Stockham {
         for (int r = 1; r < Rp; ++r) v[s + r * S] = INV ? cmulc(v[s + r * S], wt[r]) : cmul(v[s + r * S], wt[r]);
       }
       Dft<Rp, INV>::run(v, s, S);
+    }
     }
     if constexpr (!LAST) {
       if (ex.single()) lane_sync<LAYOUT, T, G>(g);  // write-after-read on the single buffer

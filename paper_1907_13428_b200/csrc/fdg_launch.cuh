@@ -296,7 +296,7 @@ cudaError_t run_hrow(cudaStream_t st, const double* in, double* out, int F, cons
                             const double* rdot, RedSlot red, const int* guard) {
   // staged full tiles; at N = 1024 only for the r.z pass, whose unstaged
   // epilogue reads of r stall (measured: 1130 -> 652 us at 128 x 1024^2)
-  if constexpr (Cfg<N>::PF_OK || N == 1024) {
+  if constexpr ((Cfg<N>::PF_OK || N == 1024) && HPlan<N, true>::SMEM <= kMaxSmem) {
     if (F % (2 * Cfg<N>::G) == 0 && (Cfg<N>::PF_OK || rdot))
       return run_hrow_v<N, true>(st, in, out, F, tw, rdot, red, guard);
   }

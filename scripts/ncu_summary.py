@@ -21,18 +21,21 @@ ALG = {"K1_row_p_update_B": 6, "K2_col_S_mid": 4, "K3_row_BT_update": 4, "P1_har
 
 def pass_name(kernel, seen):
     k = kernel.split("(")[0]
+    prev = seen.get("prev", "")
+    seen["prev"] = k
+    if "k_rowq" in k:
+        return "K1_row_p_update_B" if ", 2>" in k else "K3_row_BT_update"
     if "k_rowc" in k or "k_row<" in k:
         return "K1_row_p_update_B" if ", 2," in k else ("K3_row_BT_update" if ", 1," in k else "row_apply")
     if "k_colc" in k or "k_col<" in k:
         return "K2_col_S_mid" if ", 2," in k else "col_acc"
     if "k_t_filter" in k:
         return "P3_t_filter"
-    if "k_hartley_row" in k:
-        seen["hr"] = seen.get("hr", 0) + 1
-        return "P1_hartley_x2" if seen["hr"] % 2 == 1 else "P5_hartley_x2_dot"
+    if "k_hartley_row" in k:  # P5 follows the second x1 pass, P1 opens the solve
+        return "P5_hartley_x2_dot" if "k_hartley_col" in prev else "P1_hartley_x2"
     if "k_hartley_col" in k:
-        seen["hc"] = seen.get("hc", 0) + 1
-        return "P2_hartley_x1" if seen["hc"] % 2 == 1 else "P4_hartley_x1"
+        # P2 follows the x2 pass, P4 the t filter (a capture window may open on P4)
+        return "P2_hartley_x1" if "k_hartley_row" in prev else "P4_hartley_x1"
     if "k_axpy_dev" in k:
         return "X_axpy"
     if "k_pfa_hrow" in k:
@@ -58,7 +61,7 @@ def full(rep, out_csv, traffic_json, shape="256 256 256", label="C2"):
     hdr, units, data = rows[0], rows[1], rows[2:]
     ix = {h: i for i, h in enumerate(hdr)}
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
-             "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+             "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3, "second": 1e6, "s": 1e6}
 
     def g(r, m):
         if m not in ix:
