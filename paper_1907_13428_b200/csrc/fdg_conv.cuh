@@ -57,12 +57,6 @@ namespace fdg {
 #ifndef FDG_C_COLLY
 #define FDG_C_COLLY 2
 #endif
-#ifndef FDG_C1024_COLLY
-#define FDG_C1024_COLLY FDG_C_COLLY
-#endif
-#ifndef FDG_C2048_COLLY
-#define FDG_C2048_COLLY FDG_C_COLLY
-#endif
 #ifndef FDG_K2_WOWN
 #define FDG_K2_WOWN 1  // S-mid column pass: second convolution's input from the owned registers + the partner's half
 #endif
@@ -636,8 +630,7 @@ struct ColCPlan {
   using C = CCfg<L>;
   // exchange layout: 1 = lane-major (sub-lane-local exchanges, __syncwarp),
   // else interleaved rows (CTA-wide barriers)
-  static constexpr int LY_SEL = L == 1024 ? FDG_C1024_COLLY : (L == 2048 ? FDG_C2048_COLLY : FDG_C_COLLY);
-  static constexpr int LY = LY_SEL == 1 ? 1 : (C::HOMO_COL ? 2 : 0);
+  static constexpr int LY = FDG_C_COLLY == 1 ? 1 : (C::HOMO_COL ? 2 : 0);
   static constexpr int W = 2 * C::G;              // columns per tile
   static constexpr int P = LY == 1 ? W + 2 : W;   // staged row pitch (bank spread)
   static constexpr int TILE = PF ? C::M * P : 0;  // doubles per staged operand
