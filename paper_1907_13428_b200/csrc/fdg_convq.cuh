@@ -26,6 +26,12 @@
 
 namespace fdg {
 
+#ifndef FDG_Q_OWN
+#define FDG_Q_OWN 1  // output combination: the sub-lane's own term from its registers
+#endif
+#ifndef FDG_Q_PRE
+#define FDG_Q_PRE 1  // MODE 2: p = z + beta d_old in a flat pre-pass (once per element instead of once per sub-lane)
+#endif
 #ifndef FDG_Q_TRIV
 #define FDG_Q_TRIV 1  // trivial factors without multiplies: residue 0's twist, the W_4^c input combination
 #endif
@@ -189,12 +195,21 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
   double acc = 0.0;
   auto own = [&](int i) { return t + 16 * (8 * half + i) + 256 * bo; };
   constexpr bool XPF = MODE == 2;
+  constexpr bool PRE = MODE == 2 && FDG_Q_PRE;      // direction update in a flat pre-pass over the tile
+  constexpr int NPRE = TILE / 2 / C::THREADS;       // double2 per thread in the pre-pass
+  static_assert(!PRE || (NPRE * 2 * C::THREADS == TILE && NPRE == HR), "pre-pass tiling");
   double2 xpre[XPF ? HR : 1];
   const bool upd_x = XPF && a.upd_x && !first;
   auto load_x = [&](int tl) {
-    const size_t rx = (size_t)(tl * 2 * G + 2 * g) * n;
+    if constexpr (PRE) {
+      const double2* gx = reinterpret_cast<const double2*>(a.xs + (size_t)tl * 2 * G * n);
 #pragma unroll
-    for (int i = 0; i < (XPF ? HR : 1); ++i) xpre[i] = make_double2(a.xs[rx + own(i)], a.xs[rx + n + own(i)]);
+      for (int k = 0; k < NPRE; ++k) xpre[k] = gx[threadIdx.x + k * C::THREADS];
+    } else {
+      const size_t rx = (size_t)(tl * 2 * G + 2 * g) * n;
+#pragma unroll
+      for (int i = 0; i < (XPF ? HR : 1); ++i) xpre[i] = make_double2(a.xs[rx + own(i)], a.xs[rx + n + own(i)]);
+    }
   };
   // TMA staging (FDG_TMA_ROWS): barrier 0 = FFT input, 1 = epilogue operands
   constexpr bool TMA = FDG_TMA_ROWS;
@@ -235,6 +250,29 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
       cp_async_wait<0>();
     }
     __syncthreads();
+    if constexpr (PRE) {
+      // p = z + beta d_old once per element (not once per sub-lane), in place
+      // in the staged tile; p and the x update leave as 16-byte stores
+      double2* pz = reinterpret_cast<double2*>(st_in);
+      const double2* pd = reinterpret_cast<const double2*>(st_in2);
+      double2* gd = reinterpret_cast<double2*>(a.dnew + (size_t)f0 * n);
+      double2* gx = reinterpret_cast<double2*>(a.xs + (size_t)f0 * n);
+#pragma unroll
+      for (int k = 0; k < NPRE; ++k) {
+        const int idx = threadIdx.x + k * C::THREADS;
+        double2 z = pz[idx];
+        if (!first) {
+          const double2 dd = pd[idx];
+          z.x += beta * dd.x;
+          z.y += beta * dd.y;
+          pz[idx] = z;
+          if (upd_x) gx[idx] = make_double2(xpre[k].x + alpha * dd.x, xpre[k].y + alpha * dd.y);
+        }
+        gd[idx] = z;
+      }
+      if (upd_x && tile + (int)gridDim.x < ntiles) load_x(tile + gridDim.x);
+      __syncthreads();
+    }
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
       double2 u = make_double2(0.0, 0.0);
@@ -242,7 +280,7 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
       for (int bb = 0; bb < NB; ++bb) {
         const int pos = t + 16 * m + 256 * bb;
         double2 z = make_double2(st_in[(2 * g) * n + pos], st_in[(2 * g + 1) * n + pos]);
-        if constexpr (MODE == 2) {
+        if constexpr (MODE == 2 && !PRE) {
           double2 dd = make_double2(0.0, 0.0);
           if (!first) {
             dd = make_double2(st_in2[(2 * g) * n + pos], st_in2[(2 * g + 1) * n + pos]);
@@ -273,7 +311,7 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
       }
       v[m] = u;
     }
-    if constexpr (XPF) {
+    if constexpr (XPF && !PRE) {
       if (upd_x && tile + (int)gridDim.x < ntiles) load_x(tile + gridDim.x);
     }
     __syncthreads();  // st_in and the epilogue staging are free
@@ -336,8 +374,18 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
 #pragma unroll
     for (int i = 0; i < HR; ++i) {
       double2 u[Q];
+#if FDG_Q_OWN
+      // the sub-lane's own term is still in registers (c is uniform over a warp)
+      const double2 mine = half ? v[i + 8] : v[i];
+#pragma unroll
+      for (int cc = 0; cc < Q; ++cc) {
+        if (cc != c) u[cc] = sm[slot<1, 256, GQ>(t + 16 * (8 * half + i), cc * G + g)];
+        else u[cc] = mine;
+      }
+#else
 #pragma unroll
       for (int cc = 0; cc < Q; ++cc) u[cc] = sm[slot<1, 256, GQ>(t + 16 * (8 * half + i), cc * G + g)];
+#endif
       y[i] = qsum_rt<Q>(u, bo);
     }
 #pragma unroll
