@@ -1,4 +1,4 @@
-# r2_prof3.sh : ncu launch lists + full captures of C2 / C3 / C4 / C1 on the TMA-staged kernels, summarised ON THE BOX
+# r2_prof3.sh : ncu launch lists + full captures of C2 / C3 / C4 / C1 on the current kernels, summarised ON THE BOX
 mkdir -p gpurun_out /tmp/reps
 for cfg in C2 C3 C4; do
   CONFIG=$cfg MAXIT=2 python scripts/prof_c2.py > gpurun_out/prof_plain_$cfg.log 2>&1 || { echo plain_failed_$cfg; continue; }
@@ -21,5 +21,5 @@ python scripts/ncu_summary.py full /tmp/reps/full_C4.ncu-rep gpurun_out/r02_ncu_
 for c in C1 C2 C3 C4; do python scripts/ncu_summary.py stalls /tmp/reps/full_$c.ncu-rep gpurun_out/r02_stalls_$(echo $c | tr A-Z a-z).txt $c > /dev/null; done
 # source-level hot spots of the dominant kernel (C2 K2) and of C1's column matvec pass
 ncu -i /tmp/reps/full_C2.ncu-rep --page source --csv --print-source cuda,sass -k regex:k_colc > gpurun_out/src_c2_k2.csv 2>&1
-ncu -i /tmp/reps/full_C2.ncu-rep --page raw --csv > gpurun_out/raw_c2.csv 2>&1
+for c in C2 C3 C4 C1; do ncu -i /tmp/reps/full_$c.ncu-rep --page raw --csv > gpurun_out/raw_$c.csv 2>&1; done
 ls -la gpurun_out
