@@ -290,7 +290,7 @@ cudaError_t launch_row_apply(cudaStream_t st, LaunchCounter* lc, const double* x
   a.tw256 = s2.tw256;
   a.twq = s2.twq;
   a.scale = scale;
-  a.tkind = tf.kind == 1 ? 1 : 0;
+  a.tkind = (tf.kind == 1 && tf.c1 != 0.0) ? 1 : 0;  // no neighbour term without a sub-diagonal
   a.tc0 = 0.0;  // folded into the x2 symbol (fdg_api.cu ax2s)
   a.tc1 = psi * tf.c1;
   a.tdir = adjoint ? +1 : -1;
@@ -320,7 +320,7 @@ cudaError_t launch_row_s_out(cudaStream_t st, LaunchCounter* lc, const double* w
   a.tw256 = s2.tw256;
   a.twq = s2.twq;
   a.scale = scale;
-  a.tkind = tf.kind == 1 ? 1 : 0;
+  a.tkind = (tf.kind == 1 && tf.c1 != 0.0) ? 1 : 0;  // no neighbour term without a sub-diagonal
   a.tc0 = 0.0;  // folded into the x2 symbol (fdg_api.cu ax2s)
   a.tc1 = psi * tf.c1;
   a.tdir = +1;
@@ -354,7 +354,7 @@ cudaError_t launch_row_fused(cudaStream_t st, LaunchCounter* lc, const double* z
   a.tw256 = s2.tw256;
   a.twq = s2.twq;
   a.scale = scale;
-  a.tkind = tf.kind == 1 ? 1 : 0;
+  a.tkind = (tf.kind == 1 && tf.c1 != 0.0) ? 1 : 0;  // no neighbour term without a sub-diagonal
   a.tc0 = 0.0;
   a.tc1 = psi * tf.c1;
   a.tdir = -1;
