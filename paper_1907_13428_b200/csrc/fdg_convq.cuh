@@ -26,6 +26,9 @@
 
 namespace fdg {
 
+#ifndef FDG_Q_TWS
+#define FDG_Q_TWS 1  // twist factors from a per-thread value and a staged W_{L/16} table
+#endif
 #ifndef FDG_Q_OWN
 #define FDG_Q_OWN 1  // output combination: the sub-lane's own term from its registers
 #endif
@@ -51,7 +54,8 @@ struct QCfg {
   static constexpr bool SYMS = L <= 1024;
   static constexpr bool OK = (Q == 4 || Q == 8) && G * LT == THREADS;
   static constexpr size_t bytes(size_t stage_doubles) {
-    return sizeof(double2) * (EXB + 256) + (SYMS ? sizeof(double) * L : 0) + sizeof(double) * stage_doubles;
+    return sizeof(double2) * (EXB + 256 + (FDG_Q_TWS ? L / 16 : 0)) + (SYMS ? sizeof(double) * L : 0) +
+           sizeof(double) * stage_doubles;
   }
 };
 
@@ -99,26 +103,40 @@ __device__ __forceinline__ double2 qsum_rt(const double2 (&u)[Q], int bo) {
 
 // Sub-lane c's 256-point convolution in place on v (input: the combined,
 // untwisted u[t + 16 m]; output: W_L^{-j c} IDFT(s_c X_c)[t + 16 m]).
+// FDG_Q_TWS: the twist W_L^{(t + 16 m) c} = W_L^{t c} W_{L/16}^{m c} from one
+// per-thread value (wtc) and a staged table of the L/16 values W_{L/16}^q
+// (cw; c is uniform over a warp, so the read is a broadcast) instead of a
+// load through L1 per element (the top stall of these passes).
 template <int L, int LAYOUT, int GQ>
 __device__ __forceinline__ void conv_q(double2 (&v)[16], Ex& ex, int t, int gs, int c, const double2* tw,
-                                       const double2* twq, const double* sym) {
+                                       const double2* twq, const double* sym, const double2* cw, double2 wtc) {
   constexpr int Q = L / 256;
   constexpr bool CACHE = FDG_TWCACHE != 0;
   // residue 0 has no twist (c is uniform over a warp)
   if (c != 0 || !FDG_Q_TRIV) {
 #pragma unroll
-    for (int m = 0; m < 16; ++m) v[m] = cmul(v[m], __ldg(&twq[(t + 16 * m) * c]));
+    for (int m = 0; m < 16; ++m) {
+      if constexpr (FDG_Q_TWS) v[m] = cmul(cmul(v[m], cw[(m * c) & (L / 16 - 1)]), wtc);
+      else v[m] = cmul(v[m], __ldg(&twq[(t + 16 * m) * c]));
+    }
   }
   double2 wc[TwCache<256, 16>::K];
   fft_lane_c<256, 16, GQ, false, LAYOUT, CACHE ? 1 : 0>(v, ex, t, gs, tw, wc);
+  // staged symbol: de-interleaved by residue (s_c contiguous), so a sub-lane's
+  // 16 threads read 16 consecutive doubles (the interleaved index Q k + c
+  // is a 4-way bank conflict)
 #pragma unroll
-  for (int m = 0; m < 16; ++m) v[m] = cscale(v[m], sym[Q * (t + 16 * m) + c]);
+  for (int m = 0; m < 16; ++m)
+    v[m] = cscale(v[m], sym[QCfg<L, true>::SYMS ? c * 256 + (t + 16 * m) : Q * (t + 16 * m) + c]);
   fft_lane_c<256, 16, GQ, true, LAYOUT, CACHE ? 2 : 0>(v, ex, t, gs, tw, wc);
   // W_L^{-j c} read as W_L^{L - j c}: distinct addresses from the forward
   // twist, so no 64-bit address stays live across the transforms
   if (c != 0 || !FDG_Q_TRIV) {
 #pragma unroll
-    for (int m = 0; m < 16; ++m) v[m] = cmul(v[m], __ldg(&twq[(L - (t + 16 * m) * c) & (L - 1)]));
+    for (int m = 0; m < 16; ++m) {
+      if constexpr (FDG_Q_TWS) v[m] = cmulc(cmulc(v[m], cw[(m * c) & (L / 16 - 1)]), wtc);
+      else v[m] = cmul(v[m], __ldg(&twq[(L - (t + 16 * m) * c) & (L - 1)]));
+    }
   }
 }
 
@@ -148,16 +166,20 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
   ex.k = 0;
   double2* tw = smem_raw + C::EXB;
   load_table(tw, a.tw256, 256);
+  double2* cw = tw + 256;  // W_{L/16}^q = W_L^{16 q}
+  if constexpr (FDG_Q_TWS) {
+    for (int i = threadIdx.x; i < L / 16; i += blockDim.x) cw[i] = __ldg(&a.twq[16 * i]);
+  }
   const double* sym;
   double* stage;
   if constexpr (C::SYMS) {
-    double* d = reinterpret_cast<double*>(tw + 256);
-    for (int i = threadIdx.x; i < L; i += blockDim.x) d[i] = __ldg(&a.sym_re[i]);
+    double* d = reinterpret_cast<double*>(tw + 256 + (FDG_Q_TWS ? L / 16 : 0));
+    for (int i = threadIdx.x; i < L; i += blockDim.x) d[(i % Q) * 256 + i / Q] = __ldg(&a.sym_re[i]);
     sym = d;
     stage = d + L;
   } else {
     sym = a.sym_re;
-    stage = reinterpret_cast<double*>(tw + 256);
+    stage = reinterpret_cast<double*>(tw + 256 + (FDG_Q_TWS ? L / 16 : 0));
   }
   pdl_trigger();
   pdl_wait();
@@ -173,6 +195,7 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
   const int c = threadIdx.x / (G * 16), g = (threadIdx.x / 16) % G, t = threadIdx.x % 16;
   const int gs = c * G + g;
   const int bo = c >> 1, half = c & 1;
+  const double2 wtc = __ldg(&a.twq[t * c]);  // W_L^{t c} (FDG_Q_TWS)
   const int F = a.nt * a.n1;
   const int ntiles = F / (2 * G);
   double2 win[NB];
@@ -355,7 +378,7 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
       }
       cp_async_commit();  // group I
     }
-    conv_q<L, 1, GQ>(v, ex, t, gs, c, tw, a.twq, sym);
+    conv_q<L, 1, GQ>(v, ex, t, gs, c, tw, a.twq, sym, cw, wtc);
     // combine across the lane's Q sub-lanes
     __syncwarp();
     double2* sm = ex.next();
