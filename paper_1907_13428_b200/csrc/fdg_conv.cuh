@@ -734,6 +734,13 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL)
     const int nxt = tile + gridDim.x;
     double* st_in = S.stage + buf * TILE;
     const double* st_u = S.stage + (2 + buf) * TILE;  // MODE 2
+    // per-slice scalars of the S mid pass, requested before the wait on the
+    // staged tile so their latency hides behind it
+    double a1_t = 0.0, im2_t = 0.0;
+    if constexpr (MODE == 2) {
+      a1_t = __ldg(&a.a1[o]);
+      im2_t = __ldg(&a.inv_m2[o]);
+    }
     double2 v[R];
     if constexpr (PF) {
       if constexpr (TMA) {
@@ -749,7 +756,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL)
       if constexpr (MODE == 2 && FDG_K2_EREG) {
         // a1 p^T p of the owned positions from the registers (saves the
         // staged re-read of p in the first epilogue)
-        const double a1 = a.a1[o];
+        const double a1 = a1_t;
 #pragma unroll
         for (int i = 0; i < HR; ++i) {
           const double2 pv = b ? v[i + HR] : v[i];
@@ -790,7 +797,7 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL)
     } else {
       // S mid pass: Bp = u + scale L1 p; w = Bp / m2[o] (-> a.w, and the
       // input of the second convolution); vp = scale L1 w + a1 p (-> a.out)
-      const double im2 = a.inv_m2[o], a1 = a.a1[o];
+      const double im2 = im2_t, a1 = a1_t;
 #pragma unroll
       for (int i = 0; i < HR; ++i) {
         const int pos = t + T * (i + b * HR);

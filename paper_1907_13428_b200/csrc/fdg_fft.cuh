@@ -212,15 +212,23 @@ __device__ __forceinline__ int lidx(int pos, int g) {
   return g * N + (pos ^ (f & 7));
 }
 
+#ifndef FDG_HIDX4_FOLD
+#define FDG_HIDX4_FOLD 1
+#endif
 // Split-interleaved slot (fdg_conv.cuh column passes, warps holding only
 // even- or only odd-half sub-lanes): rows of G lanes whose two halves (G/2
 // sub-lanes each) are swapped on rows of odd popcount, so the 32/(G/2)
 // positions a half-row warp touches always fill complementary halves of the
 // 128-byte bank window (any power-of-two position pattern has half of its
 // positions at odd popcount).
+// G = 4 (rows of 64 bytes, two per bank window): the first Stockham scatter
+// writes pos = 16 t + r for consecutive t, whose row parity never changes, so
+// bit 4 of pos is folded into the row's low bit as well (ncu: 8 -> 4
+// wavefronts per store of that scatter at L = 2048).
 template <int G>
 __device__ __forceinline__ int hidx(int pos, int g) {
-  return pos * G + (g ^ ((__popc(pos) & 1) * (G / 2)));
+  const int row = (G == 4 && FDG_HIDX4_FOLD) ? (pos ^ ((pos >> 4) & 1)) : pos;
+  return row * G + (g ^ ((__popc(pos) & 1) * (G / 2)));
 }
 
 // LAYOUT 0: lane-interleaved rows of G (column passes); 1: lane-major;
