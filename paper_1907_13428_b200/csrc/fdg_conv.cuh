@@ -175,7 +175,10 @@ struct CSmem {
     }
     if constexpr (SR) {
       double* d = reinterpret_cast<double*>(t);
-      for (int i = threadIdx.x; i < L; i += blockDim.x) d[i] = __ldg(&gsym_re[i]);
+      // de-interleaved: even-frequency half | odd-frequency half (a sub-lane's
+      // threads then read consecutive doubles; index 2 k + b is a 2-way bank
+      // conflict in the lane-major row passes)
+      for (int i = threadIdx.x; i < L; i += blockDim.x) d[(i & 1) * (L / 2) + (i >> 1)] = __ldg(&gsym_re[i]);
       sym.re = d;
       sym.c = nullptr;
       stage = d + L;
@@ -283,7 +286,7 @@ __device__ __forceinline__ void conv_half(double2 (&v)[CCfg<L>::R], Ex& ex, int 
   double2 wc[TwCache<M, R>::K];
   fft_lane_c<M, R, G2, false, LAYOUT, CACHE ? 1 : 0>(v, ex, t, gs, tw, wc);
 #pragma unroll
-  for (int m = 0; m < R; ++m) v[m] = sym.apply(v[m], 2 * (t + T * m) + b);
+  for (int m = 0; m < R; ++m) v[m] = sym.apply(v[m], SR ? b * M + (t + T * m) : 2 * (t + T * m) + b);
   fft_lane_c<M, R, G2, true, LAYOUT, CACHE ? 2 : 0>(v, ex, t, gs, tw, wc);
   // FDG_BAL_TWIST: the odd half's post-twist W_L^-j is applied in
   // conv_combine, each half twisting the odd values of its own positions

@@ -212,6 +212,9 @@ __device__ __forceinline__ int lidx(int pos, int g) {
   return g * N + (pos ^ (f & 7));
 }
 
+#ifndef FDG_MIRROR_PLAIN
+#define FDG_MIRROR_PLAIN 1
+#endif
 #ifndef FDG_HIDX4_FOLD
 #define FDG_HIDX4_FOLD 1
 #endif
@@ -462,6 +465,17 @@ __device__ __forceinline__ void fft_lane_c(double2 (&v)[R], Ex& ex, int t, int g
   Stockham<N, R, G, INV, 1, LAYOUT, 0, CM>::run(v, ex, t, g, tw, wc);
 }
 
+// Slot of the mirror exchanges (write at pos, read at N - pos): no swizzle.
+// Ascending and descending runs of consecutive positions are both free of
+// bank conflicts in the plain layouts, while the Stockham swizzles make the
+// descending run collide across its 8-position blocks (ncu: 2x wavefronts).
+template <int LAYOUT, int N, int G>
+__device__ __forceinline__ int mslot(int pos, int g) {
+  if constexpr (!FDG_MIRROR_PLAIN) return slot<LAYOUT, N, G>(pos, g);
+  else if constexpr (LAYOUT == 1) return g * N + pos;
+  else return pos * G + g;
+}
+
 // Exchange helper: value at position (N - pos) mod N for every register
 // (used by the Hartley post-processing).  One barrier (lane_sync).
 template <int N, int R, int G, int LAYOUT = 0>
@@ -470,13 +484,13 @@ __device__ __forceinline__ void mirror_lane(const double2 (&v)[R], double2 (&w)[
   if (ex.single()) lane_sync<LAYOUT, T, G>(g);
   double2* sm = ex.next();
 #pragma unroll
-  for (int m = 0; m < R; ++m) sm[slot<LAYOUT, N, G>(t + m * T, g)] = v[m];
+  for (int m = 0; m < R; ++m) sm[mslot<LAYOUT, N, G>(t + m * T, g)] = v[m];
   lane_sync<LAYOUT, T, G>(g);
 #pragma unroll
   for (int m = 0; m < R; ++m) {
     const int pos = t + m * T;
     const int mp = (N - pos) & (N - 1);
-    w[m] = sm[slot<LAYOUT, N, G>(mp, g)];
+    w[m] = sm[mslot<LAYOUT, N, G>(mp, g)];
   }
 }
 
@@ -496,12 +510,12 @@ __device__ __forceinline__ void hartley_lane(double2 (&v)[R], Ex& ex, int t, int
   if (ex.single()) lane_sync<LAYOUT, T, G>(g);
   double2* sm = ex.next();
 #pragma unroll
-  for (int m = 0; m < R; ++m) sm[slot<LAYOUT, N, G>(t + m * T, g)] = v[m];
+  for (int m = 0; m < R; ++m) sm[mslot<LAYOUT, N, G>(t + m * T, g)] = v[m];
   lane_sync<LAYOUT, T, G>(g);
 #pragma unroll
   for (int m = 0; m < R; ++m) {
     const int mp = (N - (t + m * T)) & (N - 1);
-    v[m] = hartley_split(v[m], sm[slot<LAYOUT, N, G>(mp, g)]);
+    v[m] = hartley_split(v[m], sm[mslot<LAYOUT, N, G>(mp, g)]);
   }
 }
 

@@ -888,7 +888,7 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(doub
     if (S.ex.single()) lane_sync<0, T, G>(g);
     double2* smz = S.ex.next();
 #pragma unroll
-    for (int m = 0; m < R; ++m) smz[slot<0, N, G>(t + m * T, g)] = v[m];
+    for (int m = 0; m < R; ++m) smz[mslot<0, N, G>(t + m * T, g)] = v[m];
     lane_sync<0, T, G>(g);
 #else
     hartley_lane<N, R, G>(v, S.ex, t, g);
@@ -919,7 +919,7 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(doub
       const double inv = 0.5 * pt.inv_total * frcp(lsa * lsb);
       const double da = lsb * inv, db = lsa * inv;  // d_a / 2, d_b / 2
       const double ds = da + db, dd = da - db;
-      const double2 zc = smz[slot<0, N, G>((N - k) & (N - 1), g)];
+      const double2 zc = smz[mslot<0, N, G>((N - k) & (N - 1), g)];
       v[m] = make_double2(fma(dd, zc.x, ds * h.x), fma(-dd, zc.y, ds * h.y));
     }
     fft_lane_c<N, R, G, true, 0, 2 * TCM>(v, S.ex, t, g, S.tw, wc);
