@@ -57,9 +57,6 @@ namespace fdg {
 #ifndef FDG_C_COLLY
 #define FDG_C_COLLY 2
 #endif
-#ifndef FDG_K2_WOWN
-#define FDG_K2_WOWN 1  // S-mid column pass: second convolution's input from the owned registers + the partner's half
-#endif
 #ifndef FDG_TMA_ROWS
 #define FDG_TMA_ROWS 1  // staged split row passes: bulk-copy (TMA) staging with mbarriers
 #endif
@@ -74,11 +71,9 @@ namespace fdg {
 // Twist factors W_L^(t + T m) = W_L^t W_32^m (T = L/32 at R = 16) formed as a
 // compile-time constant multiply times one per-thread value instead of a table
 // load per element, where the table is not in shared memory (M = 1024: loads
-// through L1; measured slower where the table is staged, C2 K2 223 -> 235 us):
-// bit 0 = the odd half's pre-twist, bit 1 = the post-twist in the combine.
-#ifndef FDG_TWIST_CONST
-#define FDG_TWIST_CONST 3
-#endif
+// through L1).  Where the table is staged the loads win (C2 K2 223 -> 235 us
+// with the constants), and at M = 1024 both the pre-twist and the combine
+// need the constants (either alone measured slower than the table).
 
 // x W_32^Q (CONJ: x conj(W_32^Q)), W_32 = exp(-2 pi i / 32), compile-time Q in [0, 16).
 template <int Q, bool CONJ>
@@ -124,8 +119,7 @@ struct CCfg {
   // leaves room for four staged tiles at L = 2048)
   static constexpr bool TWS = M <= 512;
   // twist by constants (needs L / T == 32)
-  static constexpr bool TWC_PRE = R == 16 && !TWS && (FDG_TWIST_CONST & 1);
-  static constexpr bool TWC_POST = R == 16 && !TWS && (FDG_TWIST_CONST & 2);
+  static constexpr bool TWC = R == 16 && !TWS;
   // exchange | M-point twiddles | twist W_L^j (j < M) | symbol (L, real or
   // complex) | staging
   static constexpr size_t bytes(size_t stage_doubles, bool sr) {
@@ -275,7 +269,7 @@ __device__ __forceinline__ void conv_half(double2 (&v)[CCfg<L>::R], Ex& ex, int 
   constexpr int M = C::M, R = C::R, T = C::T, G2 = C::G2;
   constexpr bool CACHE = FDG_TWCACHE && TwCache<M, R>::OK;
   if (b) {
-    if constexpr (C::TWC_PRE) {
+    if constexpr (C::TWC) {
       const double2 wt = twist[t];
       twist_const<0>(v, wt);
     } else {
@@ -337,7 +331,7 @@ __device__ __forceinline__ void conv_combine(const double2 (&v)[CCfg<L>::R], dou
     sm[slot<LAYOUT, M, G2>(t + T * (b ? i : i + HR), mp.gs)] = val;
   }
   pair_sync<L, LAYOUT, HM>(mp.g);
-  if constexpr (C::TWC_POST && FDG_BAL_TWIST) {
+  if constexpr (C::TWC && FDG_BAL_TWIST) {
     combine_const<0, L, LAYOUT>(v, y, sm, mp, twist[t]);
   } else {
 #pragma unroll
@@ -830,7 +824,6 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL)
 #pragma unroll
       for (int i = 0; i < HR; ++i) sm[slot<LY, M, G2>(t + T * (i + b * HR), mp.gs)] = y[i];
       pair_sync<L, LY, Cf::HOMO_COL>(mp.g);
-#if FDG_K2_WOWN
       // the owned half of w is still in registers: only the partner's half
       // comes back from the exchange
 #pragma unroll
@@ -839,11 +832,6 @@ __global__ void __launch_bounds__(CCfg<L>::THREADS, CCfg<L>::MINB_COL)
         v[i] = b ? other : y[i];
         v[i + HR] = b ? y[i] : other;
       }
-#else
-      const int id0 = mp.half_id(0), id1 = mp.half_id(1);
-#pragma unroll
-      for (int m = 0; m < R; ++m) v[m] = sm[slot<LY, M, G2>(t + T * m, m < HR ? id0 : id1)];
-#endif
       // write-after-read across the halves: each half reads the other's
       // slots above, and the first scatter of its transform below is guarded
       // only by its own half barrier (lane_sync), so a lagging half could

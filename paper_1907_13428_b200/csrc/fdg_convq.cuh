@@ -26,19 +26,6 @@
 
 namespace fdg {
 
-#ifndef FDG_Q_TWS
-#define FDG_Q_TWS 1  // twist factors from a per-thread value and a staged W_{L/16} table
-#endif
-#ifndef FDG_Q_OWN
-#define FDG_Q_OWN 1  // output combination: the sub-lane's own term from its registers
-#endif
-#ifndef FDG_Q_PRE
-#define FDG_Q_PRE 1  // MODE 2: p = z + beta d_old in a flat pre-pass (once per element instead of once per sub-lane)
-#endif
-#ifndef FDG_Q_TRIV
-#define FDG_Q_TRIV 1  // trivial factors without multiplies: residue 0's twist, the W_4^c input combination
-#endif
-
 template <int L, bool ROWS>
 struct QCfg {
   static constexpr int Q = L >= 1024 ? L / 256 : 4;  // sub-lanes per lane (other L: unused)
@@ -54,7 +41,7 @@ struct QCfg {
   static constexpr bool SYMS = L <= 1024;
   static constexpr bool OK = (Q == 4 || Q == 8) && G * LT == THREADS;
   static constexpr size_t bytes(size_t stage_doubles) {
-    return sizeof(double2) * (EXB + 256 + (FDG_Q_TWS ? L / 16 : 0)) + (SYMS ? sizeof(double) * L : 0) +
+    return sizeof(double2) * (EXB + 256 + L / 16) + (SYMS ? sizeof(double) * L : 0) +
            sizeof(double) * stage_doubles;
   }
 };
@@ -103,7 +90,7 @@ __device__ __forceinline__ double2 qsum_rt(const double2 (&u)[Q], int bo) {
 
 // Sub-lane c's 256-point convolution in place on v (input: the combined,
 // untwisted u[t + 16 m]; output: W_L^{-j c} IDFT(s_c X_c)[t + 16 m]).
-// FDG_Q_TWS: the twist W_L^{(t + 16 m) c} = W_L^{t c} W_{L/16}^{m c} from one
+// The twist W_L^{(t + 16 m) c} = W_L^{t c} W_{L/16}^{m c} from one
 // per-thread value (wtc) and a staged table of the L/16 values W_{L/16}^q
 // (cw; c is uniform over a warp, so the read is a broadcast) instead of a
 // load through L1 per element (the top stall of these passes).
@@ -113,11 +100,10 @@ __device__ __forceinline__ void conv_q(double2 (&v)[16], Ex& ex, int t, int gs, 
   constexpr int Q = L / 256;
   constexpr bool CACHE = FDG_TWCACHE != 0;
   // residue 0 has no twist (c is uniform over a warp)
-  if (c != 0 || !FDG_Q_TRIV) {
+  if (c != 0) {
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
-      if constexpr (FDG_Q_TWS) v[m] = cmul(cmul(v[m], cw[(m * c) & (L / 16 - 1)]), wtc);
-      else v[m] = cmul(v[m], __ldg(&twq[(t + 16 * m) * c]));
+      v[m] = cmul(cmul(v[m], cw[(m * c) & (L / 16 - 1)]), wtc);
     }
   }
   double2 wc[TwCache<256, 16>::K];
@@ -131,11 +117,10 @@ __device__ __forceinline__ void conv_q(double2 (&v)[16], Ex& ex, int t, int gs, 
   fft_lane_c<256, 16, GQ, true, LAYOUT, CACHE ? 2 : 0>(v, ex, t, gs, tw, wc);
   // W_L^{-j c} read as W_L^{L - j c}: distinct addresses from the forward
   // twist, so no 64-bit address stays live across the transforms
-  if (c != 0 || !FDG_Q_TRIV) {
+  if (c != 0) {
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
-      if constexpr (FDG_Q_TWS) v[m] = cmulc(cmulc(v[m], cw[(m * c) & (L / 16 - 1)]), wtc);
-      else v[m] = cmul(v[m], __ldg(&twq[(L - (t + 16 * m) * c) & (L - 1)]));
+      v[m] = cmulc(cmulc(v[m], cw[(m * c) & (L / 16 - 1)]), wtc);
     }
   }
 }
@@ -167,19 +152,17 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
   double2* tw = smem_raw + C::EXB;
   load_table(tw, a.tw256, 256);
   double2* cw = tw + 256;  // W_{L/16}^q = W_L^{16 q}
-  if constexpr (FDG_Q_TWS) {
-    for (int i = threadIdx.x; i < L / 16; i += blockDim.x) cw[i] = __ldg(&a.twq[16 * i]);
-  }
+  for (int i = threadIdx.x; i < L / 16; i += blockDim.x) cw[i] = __ldg(&a.twq[16 * i]);
   const double* sym;
   double* stage;
   if constexpr (C::SYMS) {
-    double* d = reinterpret_cast<double*>(tw + 256 + (FDG_Q_TWS ? L / 16 : 0));
+    double* d = reinterpret_cast<double*>(tw + 256 + L / 16);
     for (int i = threadIdx.x; i < L; i += blockDim.x) d[(i % Q) * 256 + i / Q] = __ldg(&a.sym_re[i]);
     sym = d;
     stage = d + L;
   } else {
     sym = a.sym_re;
-    stage = reinterpret_cast<double*>(tw + 256 + (FDG_Q_TWS ? L / 16 : 0));
+    stage = reinterpret_cast<double*>(tw + 256 + L / 16);
   }
   pdl_trigger();
   pdl_wait();
@@ -195,7 +178,7 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
   const int c = threadIdx.x / (G * 16), g = (threadIdx.x / 16) % G, t = threadIdx.x % 16;
   const int gs = c * G + g;
   const int bo = c >> 1, half = c & 1;
-  const double2 wtc = __ldg(&a.twq[t * c]);  // W_L^{t c} (FDG_Q_TWS)
+  const double2 wtc = __ldg(&a.twq[t * c]);  // W_L^{t c}
   const int F = a.nt * a.n1;
   const int ntiles = F / (2 * G);
   double2 win[NB];
@@ -218,7 +201,7 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
   double acc = 0.0;
   auto own = [&](int i) { return t + 16 * (8 * half + i) + 256 * bo; };
   constexpr bool XPF = MODE == 2;
-  constexpr bool PRE = MODE == 2 && FDG_Q_PRE;      // direction update in a flat pre-pass over the tile
+  constexpr bool PRE = MODE == 2;                   // direction update in a flat pre-pass over the tile
   constexpr int NPRE = TILE / 2 / C::THREADS;       // double2 per thread in the pre-pass
   static_assert(!PRE || (NPRE * 2 * C::THREADS == TILE && NPRE == HR), "pre-pass tiling");
   double2 xpre[XPF ? HR : 1];
@@ -320,7 +303,7 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
             }
           }
         }
-        if constexpr (Q == 4 && FDG_Q_TRIV) {
+        if constexpr (Q == 4) {
           // W_4^c: a quarter-turn count, by one swap and two signed adds
           if (bb == 0) {
             u = z;
@@ -397,7 +380,6 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
 #pragma unroll
     for (int i = 0; i < HR; ++i) {
       double2 u[Q];
-#if FDG_Q_OWN
       // the sub-lane's own term is still in registers (c is uniform over a warp)
       const double2 mine = half ? v[i + 8] : v[i];
 #pragma unroll
@@ -405,10 +387,6 @@ __global__ void __launch_bounds__(QCfg<L, true>::THREADS, 2) k_rowq(RowArgs a) {
         if (cc != c) u[cc] = sm[slot<1, 256, GQ>(t + 16 * (8 * half + i), cc * G + g)];
         else u[cc] = mine;
       }
-#else
-#pragma unroll
-      for (int cc = 0; cc < Q; ++cc) u[cc] = sm[slot<1, 256, GQ>(t + 16 * (8 * half + i), cc * G + g)];
-#endif
       y[i] = qsum_rt<Q>(u, bo);
     }
 #pragma unroll

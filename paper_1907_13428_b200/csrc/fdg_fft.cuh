@@ -212,12 +212,6 @@ __device__ __forceinline__ int lidx(int pos, int g) {
   return g * N + (pos ^ (f & 7));
 }
 
-#ifndef FDG_MIRROR_PLAIN
-#define FDG_MIRROR_PLAIN 1
-#endif
-#ifndef FDG_HIDX4_FOLD
-#define FDG_HIDX4_FOLD 1
-#endif
 // Split-interleaved slot (fdg_conv.cuh column passes, warps holding only
 // even- or only odd-half sub-lanes): rows of G lanes whose two halves (G/2
 // sub-lanes each) are swapped on rows of odd popcount, so the 32/(G/2)
@@ -230,7 +224,7 @@ __device__ __forceinline__ int lidx(int pos, int g) {
 // wavefronts per store of that scatter at L = 2048).
 template <int G>
 __device__ __forceinline__ int hidx(int pos, int g) {
-  const int row = (G == 4 && FDG_HIDX4_FOLD) ? (pos ^ ((pos >> 4) & 1)) : pos;
+  const int row = G == 4 ? (pos ^ ((pos >> 4) & 1)) : pos;
   return row * G + (g ^ ((__popc(pos) & 1) * (G / 2)));
 }
 
@@ -340,9 +334,6 @@ struct TwCache {
 // W_N^(b r) = (W_N^t)^r W_16^(s r): the Rp - 1 per-thread values are loaded
 // once and the rest are compile-time constant multiplies (the shared-memory
 // pipe, not FP64, is the busier unit: 3 loads instead of 12 at N = 1024).
-#ifndef FDG_TW_LASTC
-#define FDG_TW_LASTC 1
-#endif
 template <int Rp, int S, bool INV, int Sx = 1, int Rx = 1>
 struct LastTwiddle {
   template <int R>
@@ -377,7 +368,7 @@ struct Stockham {
   __device__ __forceinline__ static void run(double2 (&v)[R], Ex& ex, int t, int g, const double2* ptw,
                                              double2 (&wc)[CK]) {
     static_assert(CM == 0 || (TwCache<N, R>::OK && CK >= TwCache<N, R>::K), "twiddle cache shape");
-    constexpr bool LASTC = FDG_TW_LASTC && LAST && Ns > 1 && S > 1 && R == 16 && CM == 0 && T <= Ns;
+    constexpr bool LASTC = LAST && Ns > 1 && S > 1 && R == 16 && CM == 0 && T <= Ns;
     if constexpr (LASTC) {
       double2 wt[Rp];
 #pragma unroll
@@ -396,37 +387,37 @@ struct Stockham {
       for (int s = 0; s < S; ++s) Dft<Rp, INV>::run(v, s, S);
     } else {
 #pragma unroll
-    for (int s = 0; s < S; ++s) {
-      const int b = t + s * T;  // butterfly index in [0, N/Rp)
-      if constexpr (Ns > 1) {
-        // Load the power-of-two twiddles w^1, w^2, w^4(, w^8) and form the
-        // others as products (3 of 7 loads for radix 8): the shared-memory
-        // pipe, not FP64, is the busiest unit of these kernels.
-        const double2* tw = ptw + OFF + (b & (Ns - 1));
-        double2 wt[Rp];
-        if constexpr (CM == 2) {
+      for (int s = 0; s < S; ++s) {
+        const int b = t + s * T;  // butterfly index in [0, N/Rp)
+        if constexpr (Ns > 1) {
+          // Load the power-of-two twiddles w^1, w^2, w^4(, w^8) and form the
+          // others as products (3 of 7 loads for radix 8): the shared-memory
+          // pipe, not FP64, is the busiest unit of these kernels.
+          const double2* tw = ptw + OFF + (b & (Ns - 1));
+          double2 wt[Rp];
+          if constexpr (CM == 2) {
 #pragma unroll
-          for (int r = 1; r < Rp; ++r) wt[r] = wc[s * Rp + r];
-        } else {
+            for (int r = 1; r < Rp; ++r) wt[r] = wc[s * Rp + r];
+          } else {
 #pragma unroll
-          for (int r = 1; r < Rp; ++r) {
-            if (FDG_TW_ALL || (r & (r - 1)) == 0) {
-              wt[r] = tw[(r - 1) * Ns];
-            } else {
-              const int lo = r & -r;
-              wt[r] = cmul(wt[lo], wt[r - lo]);
+            for (int r = 1; r < Rp; ++r) {
+              if (FDG_TW_ALL || (r & (r - 1)) == 0) {
+                wt[r] = tw[(r - 1) * Ns];
+              } else {
+                const int lo = r & -r;
+                wt[r] = cmul(wt[lo], wt[r - lo]);
+              }
+            }
+            if constexpr (CM == 1) {
+#pragma unroll
+              for (int r = 1; r < Rp; ++r) wc[s * Rp + r] = wt[r];
             }
           }
-          if constexpr (CM == 1) {
 #pragma unroll
-            for (int r = 1; r < Rp; ++r) wc[s * Rp + r] = wt[r];
-          }
+          for (int r = 1; r < Rp; ++r) v[s + r * S] = INV ? cmulc(v[s + r * S], wt[r]) : cmul(v[s + r * S], wt[r]);
         }
-#pragma unroll
-        for (int r = 1; r < Rp; ++r) v[s + r * S] = INV ? cmulc(v[s + r * S], wt[r]) : cmul(v[s + r * S], wt[r]);
+        Dft<Rp, INV>::run(v, s, S);
       }
-      Dft<Rp, INV>::run(v, s, S);
-    }
     }
     if constexpr (!LAST) {
       if (ex.single()) lane_sync<LAYOUT, T, G>(g);  // write-after-read on the single buffer
@@ -471,8 +462,7 @@ __device__ __forceinline__ void fft_lane_c(double2 (&v)[R], Ex& ex, int t, int g
 // descending run collide across its 8-position blocks (ncu: 2x wavefronts).
 template <int LAYOUT, int N, int G>
 __device__ __forceinline__ int mslot(int pos, int g) {
-  if constexpr (!FDG_MIRROR_PLAIN) return slot<LAYOUT, N, G>(pos, g);
-  else if constexpr (LAYOUT == 1) return g * N + pos;
+  if constexpr (LAYOUT == 1) return g * N + pos;
   else return pos * G + g;
 }
 

@@ -55,9 +55,6 @@ namespace fdg {
 #ifndef FDG_T512_DB
 #define FDG_T512_DB 0
 #endif
-#ifndef FDG_TF_CPLX
-#define FDG_TF_CPLX 1  // t filter: complex FFT, one mirror exchange, inverse FFT (0: two Hartley transforms)
-#endif
 #ifndef FDG_PF_MAX
 #define FDG_PF_MAX 512  // largest length with staged (cp.async) full-tile variants
 #endif
@@ -872,14 +869,12 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(doub
       for (int m = 0; m < R; ++m)
         v[m] = vc ? col_get<false>(data + (size_t)(t + m * T) * C + c, C, c) : make_double2(0.0, 0.0);
     }
-    // both transforms are forward Hartley transforms of the same length; the
-    // second could reuse the first one's per-thread twiddles (TwCache), but
-    // the cache pushes this kernel over its 168-register bound (measured:
-    // spills, no gain), so it is off here
+    // the inverse transform could reuse the forward one's per-thread twiddles
+    // (TwCache), but the cache pushes this kernel over its 168-register bound
+    // (measured: spills, no gain), so it is off here
     constexpr int TCM = 0;
     double2 wc[TwCache<N, R>::K];
     fft_lane_c<N, R, G, false, 0, TCM>(v, S.ex, t, g, S.tw, wc);
-#if FDG_TF_CPLX
     // Z = A + iB (spectra of the two packed real columns a, b).  The filters
     // d_a, d_b are real and even in k, so with Zc = conj(Z[N - k]) = A - iB
     //   Y = d_a A + i d_b B = (d_a + d_b)/2 Z + (d_a - d_b)/2 Zc
@@ -890,9 +885,6 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(doub
 #pragma unroll
     for (int m = 0; m < R; ++m) smz[mslot<0, N, G>(t + m * T, g)] = v[m];
     lane_sync<0, T, G>(g);
-#else
-    hartley_lane<N, R, G>(v, S.ex, t, g);
-#endif
     // spatial eigenvalue sums of the two packed columns
     double2 sa = make_double2(0.0, 0.0), sb = make_double2(0.0, 0.0);
     if (vc) {
@@ -915,7 +907,6 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(doub
       const double lsa = pt.base + (bax * bax + bay * bay) * pt.inv_m2;
       const double lsb = pt.base + (bbx * bbx + bby * bby) * pt.inv_m2;
       // one reciprocal for both columns
-#if FDG_TF_CPLX
       const double inv = 0.5 * pt.inv_total * frcp(lsa * lsb);
       const double da = lsb * inv, db = lsa * inv;  // d_a / 2, d_b / 2
       const double ds = da + db, dd = da - db;
@@ -923,13 +914,6 @@ __global__ void __launch_bounds__(Cfg<N>::THREADS, Cfg<N>::MINB) k_t_filter(doub
       v[m] = make_double2(fma(dd, zc.x, ds * h.x), fma(-dd, zc.y, ds * h.y));
     }
     fft_lane_c<N, R, G, true, 0, 2 * TCM>(v, S.ex, t, g, S.tw, wc);
-#else
-      const double inv = pt.inv_total * frcp(lsa * lsb);
-      v[m] = make_double2(h.x * (lsb * inv), h.y * (lsa * inv));
-    }
-    fft_lane_c<N, R, G, false, 0, 2 * TCM>(v, S.ex, t, g, S.tw, wc);
-    hartley_lane<N, R, G>(v, S.ex, t, g);
-#endif
 #pragma unroll
     for (int m = 0; m < R; ++m)
       if (vc) col_put<PF>(data + (size_t)(t + m * T) * C + c, C, c, v[m]);
