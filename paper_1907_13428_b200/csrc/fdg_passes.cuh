@@ -554,6 +554,17 @@ __global__ void __launch_bounds__(Cfg<L>::THREADS, Cfg<L>::MINB) k_col(ColArgs a
         v[m] = (m < H && pos < n && vc) ? col_get<false>(a.x + base + (size_t)pos * C, C, c)
                                         : make_double2(0.0, 0.0);
       }
+      if constexpr (MODE == 0) {
+        // the epilogue's accumulate operand: ask L2 for it now (a quarter of
+        // the unstaged pass's stall samples sat on those loads)
+        if (a.acc && vc) {
+#pragma unroll
+          for (int m = 0; m < H; ++m) {
+            const int pos = t + m * T;
+            if (pos < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.acc + base + (size_t)pos * C));
+          }
+        }
+      }
     }
     fft_lane<L, R, G, false>(v, S.ex, t, g, S.tw);
 #pragma unroll
