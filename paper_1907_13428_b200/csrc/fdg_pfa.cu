@@ -28,6 +28,8 @@
 // tile (2G fibres, cp.async) + one exchange area (G lanes), 224 KB.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "fdg_fft.cuh"
 #include "fdg_internal.h"
 #include "fdg_launch.cuh"
@@ -120,8 +122,12 @@ __device__ __forceinline__ void dft_odd(const double2 (&x)[P], Put&& put) {
       put(m, make_double2(A.x + B.y, A.y - B.x));
       put(P - m, make_double2(A.x - B.y, A.y + B.x));
     };
-#pragma unroll 1
-    for (int m = 1; m <= 7; ++m) {
+    // one basic block per output pair with compile-time m: the cos / sin
+    // factors become constant-bank operands of the FMAs (the run-time m of the
+    // rolled loop cost an LDC per factor: 30% of the pass's stall samples),
+    // and ptxas still cannot interleave the pairs (which spilled)
+    auto pair = [&](auto mc) {
+      constexpr int m = decltype(mc)::value;
       double2 A, B, A2, B2;
       one(m, A, B);
       one(m + 8, A2, B2);
@@ -132,6 +138,18 @@ __device__ __forceinline__ void dft_odd(const double2 (&x)[P], Put&& put) {
       }
       out(m, A, B);
       out(m + 8, A2, B2);
+    };
+#pragma unroll 1
+    for (int m = 1; m <= 7; ++m) {
+      switch (m) {
+        case 1: pair(std::integral_constant<int, 1>{}); break;
+        case 2: pair(std::integral_constant<int, 2>{}); break;
+        case 3: pair(std::integral_constant<int, 3>{}); break;
+        case 4: pair(std::integral_constant<int, 4>{}); break;
+        case 5: pair(std::integral_constant<int, 5>{}); break;
+        case 6: pair(std::integral_constant<int, 6>{}); break;
+        default: pair(std::integral_constant<int, 7>{}); break;
+      }
     }
     {
       double2 A, B;
@@ -352,16 +370,21 @@ __global__ void __launch_bounds__(PCfg<PG>::THREADS, PCfg<PG>::MINB)
   double2* E = Ex + gl * PN;
   const int ncb = (C + PW - 1) / PW;
   const long ntiles = (long)nt * ncb;
+  constexpr int CRT = PTHREADS / PW;           // tile rows covered per step of the copy loops
+  const int cj = tid % PW, cr = tid / PW;      // copy loops: column and first row of the thread
   auto stage = [&](long tile) {
     const long o = tile / ncb;
     const int c0 = (int)(tile - o * ncb) * PW;
     const int nc = C - c0 < PW ? C - c0 : PW;
     const double* src = data + o * PN * (long)C + c0;
-    for (int i = tid; i < PN * PW; i += PTHREADS) {
-      const int pos = i / PW, j = i - pos * PW;
-      if (j < nc) {
-        const unsigned d = (unsigned)__cvta_generic_to_shared(S + i);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src + (long)pos * C + j));
+    // thread -> (column cj, rows cr, cr + CRT, ...): no index division per element
+    if (cr < CRT && cj < nc) {
+      const double* sp = src + (long)cr * C + cj;
+      unsigned d = (unsigned)__cvta_generic_to_shared(S + cr * PW + cj);
+      for (int pos = cr; pos < PN; pos += CRT) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(sp));
+        sp += (long)CRT * C;
+        d += CRT * PW * (unsigned)sizeof(double);
       }
     }
   };
@@ -446,9 +469,14 @@ __global__ void __launch_bounds__(PCfg<PG>::THREADS, PCfg<PG>::MINB)
     __syncthreads();
     {
       double* dst = data + o * PN * (long)C + c0;
-      for (int i = tid; i < PN * PW; i += PTHREADS) {
-        const int pos = i / PW, j = i - pos * PW;
-        if (j < nc) dst[(long)pos * C + j] = Et[i];
+      if (cr < CRT && cj < nc) {
+        double* dp = dst + (long)cr * C + cj;
+        const double* ep = Et + cr * PW + cj;
+        for (int pos = cr; pos < PN; pos += CRT) {
+          *dp = *ep;
+          dp += (long)CRT * C;
+          ep += CRT * PW;
+        }
       }
     }
     __syncthreads();  // E reads done before the next tile's pass A
